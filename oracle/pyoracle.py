@@ -1,0 +1,219 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes access to the CPU checkers.
+
+``Checker('orc')`` loads oracle/liboracle.so (the committed plain-C
+restatement); ``Checker('ref')`` loads oracle/_ref/libtopmg_ref.so (the
+unmodified reference compiled from /root/reference by oracle/Makefile). Both
+export the same function set (topmg_oracle.h / ref_shim.cpp). Only tests/,
+__graft_entry__.smoke() and bench.py's CPU legs import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import pathlib
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+PATHS = {"orc": HERE / "liboracle.so", "ref": HERE / "_ref" / "libtopmg_ref.so"}
+
+_D = C.POINTER(C.c_double)
+_I = C.POINTER(C.c_int)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg, row=-1):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+        self.msg = msg
+        self.row = row
+
+
+def available(kind: str) -> bool:
+    return PATHS[kind].exists()
+
+
+def _d(a):
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_D)
+
+
+def _i(a):
+    assert a.dtype == np.int32 and a.flags.c_contiguous
+    return a.ctypes.data_as(_I)
+
+
+_cache = {}
+
+
+def lib(kind: str):
+    if kind in _cache:
+        return _cache[kind]
+    L = C.CDLL(str(PATHS[kind]))
+    p = kind + "_"
+    sig = {
+        "element_stiffness": (None, [C.c_double, C.c_double, _D]),
+        "system_create": (C.c_void_p, [C.c_int, C.c_int, _D, C.c_double, _I, C.c_int, _I, _D, C.c_int,
+                                       C.c_char_p, C.c_int, _I]),
+        "system_build_mg": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_char_p, C.c_int, _I]),
+        "system_num_levels": (C.c_int, [C.c_void_p]),
+        "system_rhs": (None, [C.c_void_p, _D]),
+        "system_level_nnz": (C.c_long, [C.c_void_p, C.c_int]),
+        "system_level_size": (C.c_int, [C.c_void_p, C.c_int]),
+        "system_level_csr": (C.c_int, [C.c_void_p, C.c_int, _I, _I, _D]),
+        "system_matvec": (C.c_int, [C.c_void_p, C.c_int, _D, _D]),
+        "system_vcycle": (C.c_int, [C.c_void_p, _D, _D, C.c_int, C.c_int, C.c_int]),
+        "system_solve": (C.c_int, [C.c_void_p, _D, _D, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, _D,
+                                   _I, _D, _I, _D, _I, C.c_char_p, C.c_int]),
+        "system_times": (None, [C.c_void_p, _D]),
+        "system_compliance": (C.c_double, [C.c_void_p, _D]),
+        "system_destroy": (None, [C.c_void_p]),
+        "element_energies": (C.c_int, [C.c_int, C.c_int, _D, C.c_double, _D]),
+        "effective_moduli": (None, [C.c_int, C.c_int, C.c_int, _D, _D, C.c_double, _D]),
+        "sensitivities": (C.c_int, [C.c_int, C.c_int, C.c_int, _D, _D, C.c_double, C.c_double, _D, _D]),
+        "filter": (C.c_int, [C.c_int, C.c_int, C.c_int, _D, C.c_int, C.c_double, _D, _D]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, p + name)
+        f.restype = res
+        f.argtypes = args
+    _cache[kind] = L
+    return L
+
+
+class System:
+    """assemble_from_moduli (+ build_multigrid_operators on demand)."""
+
+    def __init__(self, kind, nx, ny, moduli, nu, fixed, loads):
+        self.kind, self.L, self.p = kind, lib(kind), kind + "_"
+        self.nx, self.ny = nx, ny
+        self.n = 2 * (nx + 1) * (ny + 1)
+        e = np.ascontiguousarray(moduli, dtype=np.float64)
+        fx = np.ascontiguousarray(fixed, dtype=np.int32)
+        ld = np.ascontiguousarray([d for d, _ in loads], dtype=np.int32)
+        lv = np.ascontiguousarray([v for _, v in loads], dtype=np.float64)
+        err = C.create_string_buffer(256)
+        st = C.c_int()
+        self.h = self._f("system_create")(nx, ny, _d(e), nu, _i(fx), len(fx), _i(ld), _d(lv), len(lv), err, 256,
+                                          C.byref(st))
+        if st.value:
+            raise OracleError(st.value, err.value.decode())
+        self.levels = 1
+
+    def _f(self, name):
+        return getattr(self.L, self.p + name)
+
+    def build_mg(self, num_coarsenings, omega=0.6):
+        err = C.create_string_buffer(256)
+        row = C.c_int(-1)
+        st = self._f("system_build_mg")(self.h, num_coarsenings, omega, err, 256, C.byref(row))
+        if st:
+            raise OracleError(st, err.value.decode(), row.value)
+        self.levels = num_coarsenings + 1
+        return self
+
+    def rhs(self):
+        b = np.empty(self.n)
+        self._f("system_rhs")(self.h, _d(b))
+        return b
+
+    def csr(self, level):
+        n = self._f("system_level_size")(self.h, level)
+        nnz = self._f("system_level_nnz")(self.h, level)
+        off = np.empty(n + 1, np.int32)
+        col = np.empty(nnz, np.int32)
+        val = np.empty(nnz)
+        st = self._f("system_level_csr")(self.h, level, _i(off), _i(col), _d(val))
+        if st:
+            raise OracleError(st, "level_csr")
+        return off, col, val
+
+    def matvec(self, level, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty_like(x)
+        st = self._f("system_matvec")(self.h, level, _d(x), _d(y))
+        if st:
+            raise OracleError(st, "matvec")
+        return y
+
+    def vcycle(self, f, u, gamma=1, pre=2, post=2):
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        u = np.array(u, dtype=np.float64, copy=True)
+        st = self._f("system_vcycle")(self.h, _d(f), _d(u), gamma, pre, post)
+        if st:
+            raise OracleError(st, "vcycle")
+        return u
+
+    def solve(self, b, tol=1e-8, max_iter=1000, gamma=1, pre=2, post=2, x0=None):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x0c = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+        x = np.empty(self.n)
+        it, cv, hl = C.c_int(), C.c_int(), C.c_int()
+        fr = C.c_double()
+        hist = np.empty(max_iter + 1)
+        err = C.create_string_buffer(256)
+        st = self._f("system_solve")(self.h, _d(b), _d(x0c), tol, max_iter, gamma, pre, post, _d(x), C.byref(it),
+                                     C.byref(fr), C.byref(cv), _d(hist), C.byref(hl), err, 256)
+        if st:
+            raise OracleError(st, err.value.decode())
+        return dict(solution=x, iterations=it.value, final_residual=fr.value, converged=bool(cv.value),
+                    residual_history=hist[: hl.value].copy())
+
+    def times(self):
+        t = np.empty(3)
+        self._f("system_times")(self.h, _d(t))
+        return dict(assemble=t[0], setup=t[1], pcg=t[2])
+
+    def compliance(self, u):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        return self._f("system_compliance")(self.h, _d(u))
+
+    def close(self):
+        if self.h:
+            self._f("system_destroy")(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def element_stiffness(kind, modulus, nu):
+    k = np.empty(64)
+    getattr(lib(kind), kind + "_element_stiffness")(modulus, nu, _d(k))
+    return k.reshape(8, 8)
+
+
+def element_energies(kind, nx, ny, u, nu):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.empty(nx * ny)
+    getattr(lib(kind), kind + "_element_energies")(nx, ny, _d(u), nu, _d(out))
+    return out
+
+
+def effective_moduli(kind, nx, ny, alpha, phase_moduli, penalty):
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    pm = np.ascontiguousarray(phase_moduli, dtype=np.float64)
+    out = np.empty(nx * ny)
+    getattr(lib(kind), kind + "_effective_moduli")(nx, ny, a.shape[1], _d(a), _d(pm), penalty, _d(out))
+    return out
+
+
+def sensitivities(kind, nx, ny, alpha, phase_moduli, penalty, nu, u):
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    pm = np.ascontiguousarray(phase_moduli, dtype=np.float64)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.empty((a.shape[1], nx * ny))
+    getattr(lib(kind), kind + "_sensitivities")(nx, ny, a.shape[1], _d(a), _d(pm), penalty, nu, _d(u), _d(out))
+    return out
+
+
+def filter_sensitivities(kind, nx, ny, alpha, phase, radius, raw):
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    raw = np.ascontiguousarray(raw, dtype=np.float64)
+    out = np.empty(nx * ny)
+    getattr(lib(kind), kind + "_filter")(nx, ny, a.shape[1], _d(a), phase, radius, _d(raw), _d(out))
+    return out

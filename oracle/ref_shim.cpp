@@ -1,0 +1,316 @@
+// TEST INFRASTRUCTURE ONLY -- never linked into the product library.
+//
+// C-ABI shim over the UNMODIFIED reference library (topopt-mg, compiled from
+// /root/reference/proj/src by oracle/Makefile into oracle/_ref/). It lets the
+// pytest suite, tests/golden/make_golden.py and bench.py's cpu_baseline /
+// --impl reference leg drive the reference's own code path:
+//   assemble_from_moduli      (proj/src/fem.cpp:181-219)
+//   build_hierarchy           (proj/src/grid.cpp:53-96)
+//   build_multigrid_operators (proj/src/solvers.cpp:460-481)
+//   mg_cycle / pcgmg_solve    (proj/src/solvers.cpp:483-530)
+//   compliance / element_energies (proj/src/fem.cpp:284-318)
+//   sensitivities / filter_sensitivities (proj/src/mto.cpp:61-117)
+// The function set and signatures are identical to oracle/topmg_oracle.h with
+// the prefix ref_ instead of orc_, so tests can swap one checker for the other.
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "topmg/density.hpp"
+#include "topmg/errors.hpp"
+#include "topmg/fem.hpp"
+#include "topmg/grid.hpp"
+#include "topmg/mto.hpp"
+#include "topmg/solvers.hpp"
+#include "topmg/sparse.hpp"
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+struct RefSystem {
+  topmg::GridLevel grid;
+  topmg::LinearSystem sys;
+  topmg::GridHierarchy hier;
+  std::unique_ptr<topmg::MultigridOperators> ops;
+  double nu = 0.3;
+  double t_assemble = 0.0, t_setup = 0.0, t_pcg = 0.0;
+};
+
+void put_err(char* err, int len, const char* msg) {
+  if (err && len > 0) {
+    std::snprintf(err, static_cast<std::size_t>(len), "%s", msg);
+  }
+}
+
+// Maps the reference exception hierarchy (include/topmg/errors.hpp:9-47) onto
+// the status codes of include/tmg_gpu.h.
+int map_exception(char* err, int len, int* row) {
+  try {
+    throw;
+  } catch (const topmg::ConfigError& e) {
+    put_err(err, len, e.what());
+    return 1;
+  } catch (const topmg::DimensionError& e) {
+    put_err(err, len, e.what());
+    return 2;
+  } catch (const topmg::DefinitenessError& e) {
+    put_err(err, len, e.what());
+    if (row) *row = e.row;
+    return 3;
+  } catch (const topmg::PreconditionerError& e) {
+    put_err(err, len, e.what());
+    return 4;
+  } catch (const topmg::SplittingError& e) {
+    put_err(err, len, e.what());
+    return 5;
+  } catch (const topmg::MultiplierError& e) {
+    put_err(err, len, e.what());
+    return 8;
+  } catch (const std::exception& e) {
+    put_err(err, len, e.what());
+    return 9;
+  }
+}
+
+const topmg::SparseSymMatrix& level_matrix(const RefSystem* s, int level) {
+  if (s->ops) return s->ops->matrices.at(static_cast<std::size_t>(level));
+  if (level != 0) throw topmg::DimensionError("no multigrid operators built");
+  return s->sys.matrix;
+}
+
+}  // namespace
+
+extern "C" {
+
+void ref_element_stiffness(double modulus, double nu, double* out64) {
+  const topmg::ElementMatrix k = topmg::element_stiffness(modulus, nu);
+  std::memcpy(out64, k.data(), 64 * sizeof(double));
+}
+
+void* ref_system_create(int nx, int ny, const double* moduli, double nu,
+                        const int* fixed, int n_fixed, const int* load_dofs,
+                        const double* load_vals, int n_loads, char* err,
+                        int errlen, int* status) {
+  try {
+    auto s = std::make_unique<RefSystem>();
+    s->grid = topmg::GridLevel{nx, ny, 2, 0};
+    s->nu = nu;
+    topmg::BoundaryConditions bc;
+    bc.fixed_dofs.assign(fixed, fixed + n_fixed);
+    for (int i = 0; i < n_loads; ++i) bc.point_loads.emplace_back(load_dofs[i], load_vals[i]);
+    std::vector<double> e(moduli, moduli + static_cast<std::size_t>(nx) * ny);
+    const auto t0 = Clock::now();
+    s->sys = topmg::assemble_from_moduli(s->grid, e, nu, bc);
+    s->t_assemble = std::chrono::duration<double>(Clock::now() - t0).count();
+    *status = 0;
+    return s.release();
+  } catch (...) {
+    *status = map_exception(err, errlen, nullptr);
+    return nullptr;
+  }
+}
+
+int ref_system_build_mg(void* h, int num_coarsenings, double omega, char* err,
+                        int errlen, int* row) {
+  auto* s = static_cast<RefSystem*>(h);
+  try {
+    s->hier = topmg::build_hierarchy(s->grid.nx, s->grid.ny, num_coarsenings, 2);
+    const auto t0 = Clock::now();
+    s->ops = std::make_unique<topmg::MultigridOperators>(
+        topmg::build_multigrid_operators(s->hier, s->sys.matrix, omega));
+    s->t_setup = std::chrono::duration<double>(Clock::now() - t0).count();
+    return 0;
+  } catch (...) {
+    s->ops.reset();
+    return map_exception(err, errlen, row);
+  }
+}
+
+int ref_system_num_levels(void* h) {
+  auto* s = static_cast<RefSystem*>(h);
+  return s->ops ? static_cast<int>(s->ops->matrices.size()) : 1;
+}
+
+void ref_system_rhs(void* h, double* out) {
+  auto* s = static_cast<RefSystem*>(h);
+  std::memcpy(out, s->sys.rhs.data(), s->sys.rhs.size() * sizeof(double));
+}
+
+long ref_system_level_nnz(void* h, int level) {
+  try {
+    return static_cast<long>(level_matrix(static_cast<RefSystem*>(h), level).nnz());
+  } catch (...) {
+    return -1;
+  }
+}
+
+int ref_system_level_size(void* h, int level) {
+  try {
+    return level_matrix(static_cast<RefSystem*>(h), level).size();
+  } catch (...) {
+    return -1;
+  }
+}
+
+int ref_system_level_csr(void* h, int level, int* offsets, int* cols, double* vals) {
+  try {
+    const topmg::SparseSymMatrix& m = level_matrix(static_cast<RefSystem*>(h), level);
+    std::memcpy(offsets, m.row_offsets().data(), m.row_offsets().size() * sizeof(int));
+    std::memcpy(cols, m.col_indices().data(), m.col_indices().size() * sizeof(int));
+    std::memcpy(vals, m.values().data(), m.values().size() * sizeof(double));
+    return 0;
+  } catch (...) {
+    return 2;
+  }
+}
+
+int ref_system_matvec(void* h, int level, const double* x, double* y) {
+  try {
+    const topmg::SparseSymMatrix& m = level_matrix(static_cast<RefSystem*>(h), level);
+    std::vector<double> xv(x, x + m.size()), yv;
+    m.multiply(xv, yv);
+    std::memcpy(y, yv.data(), yv.size() * sizeof(double));
+    return 0;
+  } catch (...) {
+    return 2;
+  }
+}
+
+int ref_system_vcycle(void* h, const double* f, double* u, int gamma, int pre,
+                      int post) {
+  auto* s = static_cast<RefSystem*>(h);
+  if (!s->ops) return 2;
+  const int n = s->grid.dof_count();
+  std::vector<double> fv(f, f + n), uv(u, u + n);
+  topmg::mg_cycle(*s->ops, s->hier.finest(), uv, fv, gamma, pre, post);
+  std::memcpy(u, uv.data(), static_cast<std::size_t>(n) * sizeof(double));
+  return 0;
+}
+
+int ref_system_solve(void* h, const double* b, const double* x0, double tol,
+                     int max_iter, int gamma, int pre, int post, double* x,
+                     int* iters, double* final_relres, int* converged,
+                     double* hist, int* hist_len, char* err, int errlen) {
+  auto* s = static_cast<RefSystem*>(h);
+  if (!s->ops) {
+    put_err(err, errlen, "multigrid operators not built");
+    return 2;
+  }
+  try {
+    const int n = s->grid.dof_count();
+    std::vector<double> bv(b, b + n), x0v;
+    if (x0) x0v.assign(x0, x0 + n);
+    topmg::SolverConfig cfg;
+    cfg.method = topmg::Method::pcgmg;
+    cfg.tol = tol;
+    cfg.max_iter = max_iter;
+    cfg.omega = s->ops->omega;
+    cfg.gamma = gamma;
+    cfg.pre_sweeps = pre;
+    cfg.post_sweeps = post;
+    cfg.num_coarsenings = s->hier.finest();
+    const topmg::SolveReport rep = topmg::pcgmg_solve(*s->ops, bv, cfg, x0 ? &x0v : nullptr);
+    std::memcpy(x, rep.solution.data(), rep.solution.size() * sizeof(double));
+    *iters = rep.iterations;
+    *final_relres = rep.final_residual;
+    *converged = rep.converged ? 1 : 0;
+    std::memcpy(hist, rep.residual_history.data(),
+                rep.residual_history.size() * sizeof(double));
+    *hist_len = static_cast<int>(rep.residual_history.size());
+    s->t_pcg = rep.seconds;
+    return 0;
+  } catch (...) {
+    return map_exception(err, errlen, nullptr);
+  }
+}
+
+// seconds of the last assemble / build_multigrid_operators / pcgmg_solve
+void ref_system_times(void* h, double* out3) {
+  auto* s = static_cast<RefSystem*>(h);
+  out3[0] = s->t_assemble;
+  out3[1] = s->t_setup;
+  out3[2] = s->t_pcg;
+}
+
+double ref_system_compliance(void* h, const double* u) {
+  auto* s = static_cast<RefSystem*>(h);
+  std::vector<double> uv(u, u + s->grid.dof_count());
+  return topmg::compliance(s->sys.matrix, uv);
+}
+
+void ref_system_destroy(void* h) { delete static_cast<RefSystem*>(h); }
+
+int ref_element_energies(int nx, int ny, const double* u, double nu, double* out) {
+  try {
+    const topmg::GridLevel g{nx, ny, 2, 0};
+    std::vector<double> uv(u, u + g.dof_count());
+    const std::vector<double> e = topmg::element_energies(g, uv, nu);
+    std::memcpy(out, e.data(), e.size() * sizeof(double));
+    return 0;
+  } catch (...) {
+    return 2;
+  }
+}
+
+namespace {
+topmg::DensityField make_density(int nx, int ny, int nphases, const double* alpha) {
+  topmg::DensityField d(nx, ny, nphases);
+  for (int e = 0; e < nx * ny; ++e) {
+    for (int i = 0; i < nphases; ++i) d.at(e, i) = alpha[static_cast<std::size_t>(e) * nphases + i];
+  }
+  return d;
+}
+}  // namespace
+
+void ref_effective_moduli(int nx, int ny, int nphases, const double* alpha,
+                          const double* phase_moduli, double penalty, double* out) {
+  const topmg::DensityField d = make_density(nx, ny, nphases, alpha);
+  topmg::MaterialModel mat;
+  mat.phase_moduli.assign(phase_moduli, phase_moduli + nphases);
+  mat.penalty = penalty;
+  const std::vector<double> e = topmg::effective_moduli(d, mat);
+  std::memcpy(out, e.data(), e.size() * sizeof(double));
+}
+
+int ref_sensitivities(int nx, int ny, int nphases, const double* alpha,
+                      const double* phase_moduli, double penalty, double nu,
+                      const double* u, double* out) {
+  try {
+    const topmg::GridLevel g{nx, ny, 2, 0};
+    const topmg::DensityField d = make_density(nx, ny, nphases, alpha);
+    topmg::MaterialModel mat;
+    mat.phase_moduli.assign(phase_moduli, phase_moduli + nphases);
+    mat.penalty = penalty;
+    mat.poisson_ratio = nu;
+    std::vector<double> uv(u, u + g.dof_count());
+    const auto s = topmg::sensitivities(uv, d, mat, g);
+    for (int i = 0; i < nphases; ++i) {
+      std::memcpy(out + static_cast<std::size_t>(i) * nx * ny, s[static_cast<std::size_t>(i)].data(),
+                  s[static_cast<std::size_t>(i)].size() * sizeof(double));
+    }
+    return 0;
+  } catch (...) {
+    return 2;
+  }
+}
+
+int ref_filter(int nx, int ny, int nphases, const double* alpha, int phase,
+               double radius, const double* raw, double* out) {
+  try {
+    const topmg::GridLevel g{nx, ny, 2, 0};
+    const topmg::DensityField d = make_density(nx, ny, nphases, alpha);
+    std::vector<double> rv(raw, raw + static_cast<std::size_t>(nx) * ny);
+    const std::vector<double> f = topmg::filter_sensitivities(rv, d, phase, radius, g);
+    std::memcpy(out, f.data(), f.size() * sizeof(double));
+    return 0;
+  } catch (...) {
+    return 2;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,37 @@
+"""B200-native pCGMG for topopt-mg (arXiv 2301.07457).
+
+The hot path -- the SIMP multi-material Q4 elasticity solve K(alpha) u = f by
+CG preconditioned with a geometric-multigrid gamma-cycle, plus the compliance,
+sensitivity and filter kernels that consume u -- runs as hand-written sm_100a
+CUDA in ``libtmg_gpu.so`` behind the C ABI of ``include/tmg_gpu.h``. This
+package is the Python mirror of the reference interface over that ABI.
+"""
+from .topmg import (  # noqa: F401
+    BoundaryConditions,
+    ConfigError,
+    CudaError,
+    DefinitenessError,
+    DimensionError,
+    GridLevel,
+    MaterialModel,
+    MultigridOperators,
+    MultiplierError,
+    NumericError,
+    PreconditionerError,
+    SolveReport,
+    SolverConfig,
+    SplittingError,
+    assemble_rhs,
+    build_multigrid_operators,
+    compliance,
+    density_checker,
+    density_iid,
+    effective_moduli,
+    element_energies,
+    element_stiffness,
+    filter_sensitivities,
+    mg_cycle,
+    pcgmg_solve,
+    sensitivities,
+    wall_boundary_conditions,
+)

@@ -1,0 +1,253 @@
+// Device-side data layout and operator "providers" of the pCGMG path.
+//
+// HBM layout:
+//  * Every level stores its node field padded with a one-node ghost ring:
+//    node (x, y), x in [-1, nx+1], y in [-1, ny+1], lives at
+//        idx(x, y) = (x + 1) * P + y + OY
+//    with OY = 8 (so the interior of every column starts 128-byte aligned)
+//    and the pitch P a multiple of 8 nodes. Columns are contiguous in y,
+//    exactly like the reference numbering x*(ny+1)+y (grid.hpp:19), so a
+//    host vector is one cudaMemcpy2D away.
+//  * A displacement field is double2 per node (u, v) = dofs (2n, 2n+1) of
+//    the reference (grid.hpp:20-22): one 16-byte vector load per node.
+//  * Ghost entries are zero in every array and no kernel writes them, so
+//    stencils need no boundary branches: a ghost element has modulus 0, a
+//    ghost node has value 0 and a zero stencil.
+//  * Fine level (matrix-free): per-element modulus E (8 B, same padded
+//    indexing, element (ex, ey) at idx(ex, ey)), per-node Dirichlet byte
+//    (low nibble: times dof 2n is listed fixed, high nibble: dof 2n+1), and
+//    the unit-modulus Ke (8x8) in constant memory.
+//  * Coarse levels: the exact Galerkin operator (1/4) P^T A P as a symmetric
+//    nine-point 2x2-block stencil, 19 doubles per node in SoA planes:
+//    [0..2] centre block (a00, a01, a11), [3..6] north (0,+1),
+//    [7..10] south-east (+1,-1), [11..14] east (+1,0), [15..18] north-east
+//    (+1,+1), each block row-major A(i, j)[c][d]. The other four neighbours
+//    are read transposed from the neighbour's planes.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tmg {
+
+constexpr int kOY = 8;
+constexpr int kStencilPlanes = 19;
+
+struct Grid {
+  int nx, ny;  // elements
+  int P;       // padded pitch (nodes)
+  long size;   // padded node count (nx + 3) * P
+  __host__ __device__ __forceinline__ long idx(int x, int y) const {
+    return static_cast<long>(x + 1) * P + y + kOY;
+  }
+};
+
+__constant__ double c_ke[64];  // unit-modulus Q4 Ke, row-major (fem.cpp:131-169)
+
+// Local corner numbering of fem.cpp:83-86: (0,0)->0, (1,0)->1, (1,1)->2, (0,1)->3
+__host__ __device__ constexpr int corner(int dx, int dy) {
+  return dy ? (dx ? 2 : 3) : (dx ? 1 : 0);
+}
+
+__device__ __forceinline__ int fixed_count(uint8_t m, int c) { return (m >> (4 * c)) & 15; }
+
+// ---------------------------------------------------------------- fine ----
+// Z (sum_e E_e Ke) Z + I_fixed applied without assembly (fem.cpp:181-219 and
+// the elimination of fem.cpp:89-106).
+struct FineOp {
+  const double* __restrict__ E;
+  const uint8_t* __restrict__ M;
+  int P;
+
+  // Contribution of one element to rows (2a, 2a+1) of the node at local
+  // corner A, given the masked 3x3 neighbourhood u[dx+1][dy+1]; (OXE, OYE)
+  // is the offset of the element's corner 0 from the node.
+  template <int A, int OXE, int OYE>
+  __device__ __forceinline__ static void elem_rows(double e, const double2 (&u)[3][3],
+                                                   double& y0, double& y1) {
+    const double2 q0 = u[OXE + 1][OYE + 1], q1 = u[OXE + 2][OYE + 1];
+    const double2 q2 = u[OXE + 2][OYE + 2], q3 = u[OXE + 1][OYE + 2];
+    constexpr int r0 = 16 * A, r1 = 16 * A + 8;
+    double s0 = c_ke[r0 + 0] * q0.x;
+    s0 = fma(c_ke[r0 + 1], q0.y, s0);
+    s0 = fma(c_ke[r0 + 2], q1.x, s0);
+    s0 = fma(c_ke[r0 + 3], q1.y, s0);
+    s0 = fma(c_ke[r0 + 4], q2.x, s0);
+    s0 = fma(c_ke[r0 + 5], q2.y, s0);
+    s0 = fma(c_ke[r0 + 6], q3.x, s0);
+    s0 = fma(c_ke[r0 + 7], q3.y, s0);
+    double s1 = c_ke[r1 + 0] * q0.x;
+    s1 = fma(c_ke[r1 + 1], q0.y, s1);
+    s1 = fma(c_ke[r1 + 2], q1.x, s1);
+    s1 = fma(c_ke[r1 + 3], q1.y, s1);
+    s1 = fma(c_ke[r1 + 4], q2.x, s1);
+    s1 = fma(c_ke[r1 + 5], q2.y, s1);
+    s1 = fma(c_ke[r1 + 6], q3.x, s1);
+    s1 = fma(c_ke[r1 + 7], q3.y, s1);
+    y0 = fma(e, s0, y0);
+    y1 = fma(e, s1, y1);
+  }
+
+  // y = (A x)_i and the diagonal of row i.
+  __device__ __forceinline__ void apply(const double2* __restrict__ x, long i, double2& y,
+                                        double2& d) const {
+    double2 u[3][3];
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx) {
+#pragma unroll
+      for (int dy = -1; dy <= 1; ++dy) {
+        const long j = i + dx * P + dy;
+        double2 v = x[j];
+        const uint8_t m = M[j];
+        if (m & 0x0F) v.x = 0.0;
+        if (m & 0xF0) v.y = 0.0;
+        u[dx + 1][dy + 1] = v;
+      }
+    }
+    const double eA = E[i - P - 1], eB = E[i - 1], eC = E[i], eD = E[i - P];
+    double y0 = 0.0, y1 = 0.0;
+    elem_rows<2, -1, -1>(eA, u, y0, y1);  // element (x-1, y-1): node is its corner 2
+    elem_rows<3, 0, -1>(eB, u, y0, y1);   // element (x,   y-1): corner 3
+    elem_rows<0, 0, 0>(eC, u, y0, y1);    // element (x,   y  ): corner 0
+    elem_rows<1, -1, 0>(eD, u, y0, y1);   // element (x-1, y  ): corner 1
+    double d0 = eA * c_ke[4 * 8 + 4];
+    d0 = fma(eB, c_ke[6 * 8 + 6], d0);
+    d0 = fma(eC, c_ke[0], d0);
+    d0 = fma(eD, c_ke[2 * 8 + 2], d0);
+    double d1 = eA * c_ke[5 * 8 + 5];
+    d1 = fma(eB, c_ke[7 * 8 + 7], d1);
+    d1 = fma(eC, c_ke[1 * 8 + 1], d1);
+    d1 = fma(eD, c_ke[3 * 8 + 3], d1);
+    const uint8_t mi = M[i];
+    const int k0 = fixed_count(mi, 0), k1 = fixed_count(mi, 1);
+    const double2 xi = x[i];
+    if (k0) {
+      y0 = k0 * xi.x;
+      d0 = k0;
+    }
+    if (k1) {
+      y1 = k1 * xi.y;
+      d1 = k1;
+    }
+    y = make_double2(y0, y1);
+    d = make_double2(d0, d1);
+  }
+
+  __device__ __forceinline__ double2 diag(long i) const {
+    const double eA = E[i - P - 1], eB = E[i - 1], eC = E[i], eD = E[i - P];
+    double d0 = eA * c_ke[4 * 8 + 4];
+    d0 = fma(eB, c_ke[6 * 8 + 6], d0);
+    d0 = fma(eC, c_ke[0], d0);
+    d0 = fma(eD, c_ke[2 * 8 + 2], d0);
+    double d1 = eA * c_ke[5 * 8 + 5];
+    d1 = fma(eB, c_ke[7 * 8 + 7], d1);
+    d1 = fma(eC, c_ke[1 * 8 + 1], d1);
+    d1 = fma(eD, c_ke[3 * 8 + 3], d1);
+    const uint8_t mi = M[i];
+    const int k0 = fixed_count(mi, 0), k1 = fixed_count(mi, 1);
+    if (k0) d0 = k0;
+    if (k1) d1 = k1;
+    return make_double2(d0, d1);
+  }
+
+  // Block A(i, i + (ex, ey)) (2x2, row-major) of the eliminated operator.
+  __device__ __forceinline__ void block(long i, int ex, int ey, double b[4]) const {
+    b[0] = b[1] = b[2] = b[3] = 0.0;
+#pragma unroll
+    for (int sx = 0; sx <= 1; ++sx) {
+#pragma unroll
+      for (int sy = 0; sy <= 1; ++sy) {
+        const int lx = 1 - sx, ly = 1 - sy;  // node's corner in element (x-1+sx, y-1+sy)
+        const int jx = lx + ex, jy = ly + ey;
+        if (jx < 0 || jx > 1 || jy < 0 || jy > 1) continue;
+        const double e = E[i - lx * P - ly];
+        const int a = corner(lx, ly), bb = corner(jx, jy);
+        b[0] = fma(e, c_ke[(2 * a) * 8 + 2 * bb], b[0]);
+        b[1] = fma(e, c_ke[(2 * a) * 8 + 2 * bb + 1], b[1]);
+        b[2] = fma(e, c_ke[(2 * a + 1) * 8 + 2 * bb], b[2]);
+        b[3] = fma(e, c_ke[(2 * a + 1) * 8 + 2 * bb + 1], b[3]);
+      }
+    }
+    const uint8_t mi = M[i], mj = M[i + ex * P + ey];
+    const int fi0 = fixed_count(mi, 0), fi1 = fixed_count(mi, 1);
+    const int fj0 = fixed_count(mj, 0), fj1 = fixed_count(mj, 1);
+    if (fi0 || fj0) b[0] = 0.0;
+    if (fi0 || fj1) b[1] = 0.0;
+    if (fi1 || fj0) b[2] = 0.0;
+    if (fi1 || fj1) b[3] = 0.0;
+    if (ex == 0 && ey == 0) {
+      if (fi0) b[0] = fi0;
+      if (fi1) b[3] = fi1;
+    }
+  }
+};
+
+// ------------------------------------------------------------- stencil ----
+struct StencilOp {
+  const double* __restrict__ S;  // kStencilPlanes planes of LS doubles
+  long LS;
+  int P;
+
+  __device__ __forceinline__ double s(int k, long i) const { return S[k * LS + i]; }
+
+  __device__ __forceinline__ void fwd(int k, long i, double2 v, double& y0, double& y1) const {
+    y0 = fma(s(k, i), v.x, y0);
+    y0 = fma(s(k + 1, i), v.y, y0);
+    y1 = fma(s(k + 2, i), v.x, y1);
+    y1 = fma(s(k + 3, i), v.y, y1);
+  }
+  // neighbour j's forward block toward i, transposed
+  __device__ __forceinline__ void bwd(int k, long j, double2 v, double& y0, double& y1) const {
+    y0 = fma(s(k, j), v.x, y0);
+    y0 = fma(s(k + 2, j), v.y, y0);
+    y1 = fma(s(k + 1, j), v.x, y1);
+    y1 = fma(s(k + 3, j), v.y, y1);
+  }
+
+  __device__ __forceinline__ void apply(const double2* __restrict__ x, long i, double2& y,
+                                        double2& d) const {
+    const double2 xc = x[i];
+    const double c00 = s(0, i), c01 = s(1, i), c11 = s(2, i);
+    double y0 = c00 * xc.x, y1 = c01 * xc.x;
+    y0 = fma(c01, xc.y, y0);
+    y1 = fma(c11, xc.y, y1);
+    fwd(3, i, x[i + 1], y0, y1);       // N
+    fwd(7, i, x[i + P - 1], y0, y1);   // SE
+    fwd(11, i, x[i + P], y0, y1);      // E
+    fwd(15, i, x[i + P + 1], y0, y1);  // NE
+    bwd(3, i - 1, x[i - 1], y0, y1);          // S  = N of (x, y-1)
+    bwd(7, i - P + 1, x[i - P + 1], y0, y1);  // NW = SE of (x-1, y+1)
+    bwd(11, i - P, x[i - P], y0, y1);         // W  = E of (x-1, y)
+    bwd(15, i - P - 1, x[i - P - 1], y0, y1); // SW = NE of (x-1, y-1)
+    y = make_double2(y0, y1);
+    d = make_double2(c00, c11);
+  }
+
+  __device__ __forceinline__ double2 diag(long i) const { return make_double2(s(0, i), s(2, i)); }
+
+  __device__ __forceinline__ void block(long i, int ex, int ey, double b[4]) const {
+    int k = -1;
+    long at = i;
+    bool tr = false;
+    if (ex == 0 && ey == 0) {
+      b[0] = s(0, i);
+      b[1] = b[2] = s(1, i);
+      b[3] = s(2, i);
+      return;
+    }
+    if (ex == 0 && ey == 1) k = 3;
+    else if (ex == 1 && ey == -1) k = 7;
+    else if (ex == 1 && ey == 0) k = 11;
+    else if (ex == 1 && ey == 1) k = 15;
+    else if (ex == 0 && ey == -1) { k = 3; at = i - 1; tr = true; }
+    else if (ex == -1 && ey == 1) { k = 7; at = i - P + 1; tr = true; }
+    else if (ex == -1 && ey == 0) { k = 11; at = i - P; tr = true; }
+    else { k = 15; at = i - P - 1; tr = true; }
+    b[0] = s(k, at);
+    b[1] = s(k + (tr ? 2 : 1), at);
+    b[2] = s(k + (tr ? 1 : 2), at);
+    b[3] = s(k + 3, at);
+  }
+};
+
+}  // namespace tmg

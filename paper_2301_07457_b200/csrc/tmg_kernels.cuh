@@ -1,0 +1,607 @@
+// sm_100a kernels of the pCGMG path. All fp64, HBM-bound stencils: no tensor
+// cores (FP64 MMA is not a Blackwell lever and the arithmetic intensity is
+// ~2-3 flop/B). See DESIGN.md section 4 for the per-kernel byte counts.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "tmg_device.cuh"
+
+namespace tmg {
+
+constexpr int kBX = 64;  // threads along y (contiguous) per block
+constexpr int kBY = 4;   // threads along x per block
+constexpr int kRedThreads = 256;
+constexpr int kRedBlocks = 148 * 8;  // fixed grid => fixed reduction order
+
+// ------------------------------------------------------------ reductions --
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum in a fixed tree order; result valid in thread 0.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[NT / 32];
+  const int t = threadIdx.x + threadIdx.y * blockDim.x;
+  v = warp_sum(v);
+  if ((t & 31) == 0) sh[t >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (t < 32) {
+    r = (t < NT / 32) ? sh[t] : 0.0;
+    r = warp_sum(r);
+  }
+  __syncthreads();
+  return r;
+}
+
+// Scalars of the PCG recurrence (pcg_solve, solvers.cpp:332-395), resident on
+// the device so iterations chain without host round trips.
+struct PcgState {
+  double bnorm;
+  double rr, zr, zr_prev, pap, alpha, beta, relres;
+  int it;      // iteration being computed (1-based)
+  int status;  // 0 ok, 4 preconditioner (zr <= 0), 3 definiteness (pAp <= 0)
+};
+
+// Mirror written by the reducing block to mapped pinned host memory.
+struct HostMirror {
+  double relres;
+  double zr, pap, rr;
+  int status;
+  int it;
+};
+
+enum RedOp { kRedNone = 0, kRedZr = 1, kRedPap = 2, kRedRr = 3, kRedB = 4, kRedPlain = 5 };
+
+// Final stage: the last block to finish sums all partials in index order.
+// Deterministic for a fixed grid: the order never depends on which block
+// arrives last.
+template <int NT>
+__device__ __forceinline__ void finish_reduction(double part, double* partials,
+                                                 unsigned* ticket, int nblocks,
+                                                 RedOp op, PcgState* st,
+                                                 HostMirror* hm, double* out) {
+  const int t = threadIdx.x + threadIdx.y * blockDim.x;
+  const int b = blockIdx.x + blockIdx.y * gridDim.x;
+  double s = block_sum<NT>(part);
+  __shared__ bool last;
+  if (t == 0) {
+    partials[b] = s;
+    __threadfence();
+    last = (atomicAdd(ticket, 1u) == static_cast<unsigned>(nblocks - 1));
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double acc = 0.0;
+  for (int k = t; k < nblocks; k += NT) acc += __ldcg(partials + k);
+  acc = block_sum<NT>(acc);
+  if (t != 0) return;
+  *ticket = 0u;
+  if (out) *out = acc;
+  if (!st) return;
+  switch (op) {
+    case kRedZr: {
+      // solvers.cpp:360-371
+      st->zr = acc;
+      if (!(acc > 0.0) && st->status == 0) st->status = 4;
+      st->beta = (st->it == 1) ? 0.0 : acc / st->zr_prev;
+      st->zr_prev = acc;
+      if (hm) hm->zr = acc;
+      break;
+    }
+    case kRedPap: {
+      // solvers.cpp:373-382
+      st->pap = acc;
+      if (!(acc > 0.0) && st->status == 0) st->status = 3;
+      st->alpha = st->zr / acc;
+      if (hm) hm->pap = acc;
+      break;
+    }
+    case kRedRr: {
+      // solvers.cpp:383-390 (norm2(r) / bnorm)
+      st->rr = acc;
+      st->relres = sqrt(acc) / st->bnorm;
+      if (hm) {
+        hm->rr = acc;
+        hm->relres = st->relres;
+        hm->status = st->status;
+        hm->it = st->it;
+      }
+      st->it += 1;
+      break;
+    }
+    case kRedB: {
+      st->bnorm = sqrt(acc);
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+// --------------------------------------------------------- node kernels --
+
+struct NodeIdx {
+  int x, y;
+  bool ok;
+};
+
+__device__ __forceinline__ NodeIdx node_of_thread(const Grid& g) {
+  NodeIdx n;
+  n.y = blockIdx.x * kBX + threadIdx.x;
+  n.x = blockIdx.y * kBY + threadIdx.y;
+  n.ok = (n.x <= g.nx) && (n.y <= g.ny);
+  return n;
+}
+
+// y = A x, optionally with partial x.y for a fused dot (K1 / K5 / K9).
+template <class Op, bool DOT>
+__global__ void __launch_bounds__(kBX* kBY) k_apply(Op op, Grid g, const double2* __restrict__ x,
+                                                    double2* __restrict__ y, double* partials,
+                                                    unsigned* ticket, RedOp rop, PcgState* st,
+                                                    HostMirror* hm, double* out) {
+  const NodeIdx n = node_of_thread(g);
+  double part = 0.0;
+  if (n.ok) {
+    const long i = g.idx(n.x, n.y);
+    double2 r, d;
+    op.apply(x, i, r, d);
+    y[i] = r;
+    if (DOT) {
+      const double2 xi = x[i];
+      part = xi.x * r.x + xi.y * r.y;
+    }
+  }
+  if (DOT) finish_reduction<kBX * kBY>(part, partials, ticket, gridDim.x * gridDim.y, rop, st, hm, out);
+}
+
+// Damped-Jacobi sweep x_out = x_in + omega D^-1 (f - A x_in) (jacobi_sweep,
+// solvers.cpp:30-37). ZERO: x_in is the zero vector (first pre-smoothing
+// sweep of a visit that starts from u = 0): x_out = omega f / D.
+template <class Op, bool ZERO>
+__global__ void __launch_bounds__(kBX* kBY) k_sweep(Op op, Grid g, const double2* __restrict__ xin,
+                                                    double2* __restrict__ xout,
+                                                    const double2* __restrict__ f, double omega) {
+  const NodeIdx n = node_of_thread(g);
+  if (!n.ok) return;
+  const long i = g.idx(n.x, n.y);
+  const double2 fi = f[i];
+  double2 ax, d;
+  if (ZERO) {
+    d = op.diag(i);
+    xout[i] = make_double2(omega * fi.x / d.x, omega * fi.y / d.y);
+  } else {
+    op.apply(xin, i, ax, d);
+    const double2 xi = xin[i];
+    xout[i] = make_double2(xi.x + omega * (fi.x - ax.x) / d.x, xi.y + omega * (fi.y - ax.y) / d.y);
+  }
+}
+
+// r = f - A x (solvers.cpp:498-499)
+template <class Op>
+__global__ void __launch_bounds__(kBX* kBY) k_residual(Op op, Grid g, const double2* __restrict__ x,
+                                                       const double2* __restrict__ f,
+                                                       double2* __restrict__ r) {
+  const NodeIdx n = node_of_thread(g);
+  if (!n.ok) return;
+  const long i = g.idx(n.x, n.y);
+  double2 ax, d;
+  op.apply(x, i, ax, d);
+  const double2 fi = f[i];
+  r[i] = make_double2(fi.x - ax.x, fi.y - ax.y);
+}
+
+// f_c = (1/4) P^T r as a gather over the 3x3 fine children of each coarse
+// node (restrict, grid.cpp:122-142). Ghost fine nodes hold 0.
+__global__ void __launch_bounds__(kBX* kBY) k_restrict(Grid cg, Grid fg, const double2* __restrict__ r,
+                                                       double2* __restrict__ fc) {
+  const NodeIdx n = node_of_thread(cg);
+  if (!n.ok) return;
+  const long c = fg.idx(2 * n.x, 2 * n.y);
+  const double w[3] = {0.5, 1.0, 0.5};
+  double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+  for (int dx = -1; dx <= 1; ++dx) {
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+      const double2 v = r[c + dx * fg.P + dy];
+      const double ww = 0.25 * w[dx + 1] * w[dy + 1];
+      s0 = fma(ww, v.x, s0);
+      s1 = fma(ww, v.y, s1);
+    }
+  }
+  fc[cg.idx(n.x, n.y)] = make_double2(s0, s1);
+}
+
+// x (+)= P u_c, bilinear (prolongate, grid.cpp:98-120 + solvers.cpp:508-509).
+template <bool ADD>
+__global__ void __launch_bounds__(kBX* kBY) k_prolong(Grid fg, Grid cg, const double2* __restrict__ uc,
+                                                      double2* __restrict__ x) {
+  const NodeIdx n = node_of_thread(fg);
+  if (!n.ok) return;
+  const int X0 = n.x >> 1, Y0 = n.y >> 1;
+  const bool ox = n.x & 1, oy = n.y & 1;
+  double s0, s1;
+  const long c = cg.idx(X0, Y0);
+  const double2 a = uc[c];
+  if (!ox && !oy) {
+    s0 = a.x;
+    s1 = a.y;
+  } else if (ox && !oy) {
+    const double2 b = uc[c + cg.P];
+    s0 = 0.5 * a.x + 0.5 * b.x;
+    s1 = 0.5 * a.y + 0.5 * b.y;
+  } else if (!ox && oy) {
+    const double2 b = uc[c + 1];
+    s0 = 0.5 * a.x + 0.5 * b.x;
+    s1 = 0.5 * a.y + 0.5 * b.y;
+  } else {
+    const double2 b = uc[c + 1], e = uc[c + cg.P], f = uc[c + cg.P + 1];
+    s0 = 0.25 * a.x + 0.25 * b.x + 0.25 * e.x + 0.25 * f.x;
+    s1 = 0.25 * a.y + 0.25 * b.y + 0.25 * e.y + 0.25 * f.y;
+  }
+  const long i = fg.idx(n.x, n.y);
+  if (ADD) {
+    const double2 xi = x[i];
+    x[i] = make_double2(xi.x + s0, xi.y + s1);
+  } else {
+    x[i] = make_double2(s0, s1);
+  }
+}
+
+// ------------------------------------------------------- Galerkin (K6) --
+
+__host__ __device__ constexpr double pw(int o) { return o == 0 ? 1.0 : 0.5; }
+
+// Coarse stencil of node (X, Y): (1/4) sum_{i,j} P(i,I) A(i,j) P(j,J)
+// (galerkin_coarse_matrix, solvers.cpp:397-458), evaluated as a gather over
+// the 3x3 fine children i of I and their 3x3 fine neighbours j; the parents
+// of j are always inside I's 3x3 coarse neighbourhood. Only the centre and the
+// four forward blocks are stored (symmetry).
+template <class Op>
+__global__ void __launch_bounds__(128) k_galerkin(Op fine, Grid fg, Grid cg, double* __restrict__ Sc,
+                                                  long LSc) {
+  const int Y = blockIdx.x * 32 + threadIdx.x;
+  const int X = blockIdx.y * 4 + threadIdx.y;
+  if (X > cg.nx || Y > cg.ny) return;
+  double acc[5][4];
+#pragma unroll
+  for (int a = 0; a < 5; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  // slot of coarse offset (ox, oy): centre 0, N 1, SE 2, E 3, NE 4, else -1
+#pragma unroll
+  for (int dx = -1; dx <= 1; ++dx) {
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+      const int fx = 2 * X + dx, fy = 2 * Y + dy;
+      if (fx < 0 || fx > fg.nx || fy < 0 || fy > fg.ny) continue;
+      const long i = fg.idx(fx, fy);
+      const double wi = 0.25 * pw(dx) * pw(dy);
+#pragma unroll
+      for (int ex = -1; ex <= 1; ++ex) {
+#pragma unroll
+        for (int ey = -1; ey <= 1; ++ey) {
+          const int jx = dx + ex, jy = dy + ey;  // fine offset of j from (2X, 2Y)
+          // parents of j along each axis: even -> one (weight 1), odd -> two (1/2)
+          const int nxp = (jx & 1) ? 2 : 1, nyp = (jy & 1) ? 2 : 1;
+          bool any = false;
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              if (a >= nxp || c >= nyp) continue;
+              const int ox = (jx & 1) ? ((jx - 1) / 2 + a) : jx / 2;
+              const int oy = (jy & 1) ? ((jy - 1) / 2 + c) : jy / 2;
+              const bool fwd = (ox == 0 && oy == 0) || (ox == 0 && oy == 1) || (ox == 1);
+              any = any || fwd;
+            }
+          if (!any) continue;
+          double b[4];
+          fine.block(i, ex, ey, b);
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              if (a >= nxp || c >= nyp) continue;
+              const int ox = (jx & 1) ? ((jx - 1) / 2 + a) : jx / 2;
+              const int oy = (jy & 1) ? ((jy - 1) / 2 + c) : jy / 2;
+              int slot = -1;
+              if (ox == 0 && oy == 0) slot = 0;
+              else if (ox == 0 && oy == 1) slot = 1;
+              else if (ox == 1 && oy == -1) slot = 2;
+              else if (ox == 1 && oy == 0) slot = 3;
+              else if (ox == 1 && oy == 1) slot = 4;
+              if (slot < 0) continue;
+              const double w = wi * ((jx & 1) ? 0.5 : 1.0) * ((jy & 1) ? 0.5 : 1.0);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) acc[slot][q] = fma(w, b[q], acc[slot][q]);
+            }
+        }
+      }
+    }
+  }
+  const long I = cg.idx(X, Y);
+  Sc[0 * LSc + I] = acc[0][0];
+  Sc[1 * LSc + I] = acc[0][1];
+  Sc[2 * LSc + I] = acc[0][3];
+#pragma unroll
+  for (int s = 1; s < 5; ++s)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Sc[(3 + 4 * (s - 1) + q) * LSc + I] = acc[s][q];
+}
+
+// ------------------------------------------------- coarsest level (K7) --
+
+// Dense coarsest matrix in the reference dof order (row-major n x n).
+template <class Op>
+__global__ void k_dense_assemble(Op op, Grid g, double* __restrict__ A, int n) {
+  const int y = blockIdx.x * blockDim.x + threadIdx.x;
+  const int x = blockIdx.y;
+  if (x > g.nx || y > g.ny) return;
+  const long i = g.idx(x, y);
+  const int ri = 2 * (x * (g.ny + 1) + y);
+  for (int ex = -1; ex <= 1; ++ex)
+    for (int ey = -1; ey <= 1; ++ey) {
+      const int x2 = x + ex, y2 = y + ey;
+      if (x2 < 0 || x2 > g.nx || y2 < 0 || y2 > g.ny) continue;
+      double b[4];
+      op.block(i, ex, ey, b);
+      const int cj = 2 * (x2 * (g.ny + 1) + y2);
+      A[static_cast<long>(ri) * n + cj] = b[0];
+      A[static_cast<long>(ri) * n + cj + 1] = b[1];
+      A[static_cast<long>(ri + 1) * n + cj] = b[2];
+      A[static_cast<long>(ri + 1) * n + cj + 1] = b[3];
+    }
+}
+
+// Right-looking Cholesky, lower triangle in place, one CTA (n <= 2048).
+// A non-positive pivot records its row like CholeskyFactor::factor
+// (solvers.cpp:144-148).
+__global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ A, int n, int* bad_row) {
+  __shared__ int fail;
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int lane = t & 31, w = t >> 5, nw = nt >> 5;
+  if (t == 0) fail = -1;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    if (t == 0) {
+      const double d = A[static_cast<long>(k) * n + k];
+      if (!(d > 0.0)) fail = k;
+      else A[static_cast<long>(k) * n + k] = sqrt(d);
+    }
+    __syncthreads();
+    if (fail >= 0) break;
+    const double piv = A[static_cast<long>(k) * n + k];
+    for (int i = k + 1 + t; i < n; i += nt) A[static_cast<long>(i) * n + k] /= piv;
+    __syncthreads();
+    for (int i = k + 1 + w; i < n; i += nw) {
+      const double lik = A[static_cast<long>(i) * n + k];
+      double* Ai = A + static_cast<long>(i) * n;
+      for (int j = k + 1 + lane; j <= i; j += 32) Ai[j] -= lik * A[static_cast<long>(j) * n + k];
+    }
+    __syncthreads();
+  }
+  if (t == 0) *bad_row = fail;
+}
+
+// Column j of L^-1 (stored as row j of LiT), one warp per column, the
+// running column kept in shared memory.
+__global__ void k_lower_inverse(const double* __restrict__ L, double* __restrict__ LiT, int n) {
+  extern __shared__ double ycol[];
+  const int wpb = blockDim.x >> 5;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * wpb + w;
+  if (j >= n) return;
+  double* yv = ycol + static_cast<long>(w) * n;
+  for (int i = lane; i < n; i += 32) yv[i] = 0.0;
+  __syncwarp();
+  if (lane == 0) yv[j] = 1.0 / L[static_cast<long>(j) * n + j];
+  __syncwarp();
+  for (int i = j + 1; i < n; ++i) {
+    const double* Li = L + static_cast<long>(i) * n;
+    double s = 0.0;
+    for (int k = j + lane; k < i; k += 32) s = fma(Li[k], yv[k], s);
+    s = warp_sum(s);
+    if (lane == 0) yv[i] = -s / Li[i];
+    __syncwarp();
+  }
+  for (int i = lane; i < n; i += 32) LiT[static_cast<long>(j) * n + i] = yv[i];
+}
+
+// Ainv = L^-T L^-1 (symmetric), Ainv[i][j] = sum_k LiT[i][k] LiT[j][k].
+__global__ void k_gram(const double* __restrict__ LiT, double* __restrict__ Ainv, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= n) return;
+  const int k0 = i > j ? i : j;
+  const double* a = LiT + static_cast<long>(i) * n;
+  const double* b = LiT + static_cast<long>(j) * n;
+  double s = 0.0;
+  for (int k = k0; k < n; ++k) s = fma(a[k], b[k], s);
+  Ainv[static_cast<long>(i) * n + j] = s;
+}
+
+// u0 = A0^-1 f0 on the coarsest grid (CholeskyFactor::solve, solvers.cpp:154).
+__global__ void k_coarse_solve(const double* __restrict__ Ainv, int n, Grid g,
+                               const double2* __restrict__ f, double2* __restrict__ u) {
+  extern __shared__ double fd[];
+  for (int k = threadIdx.x; k < n / 2; k += blockDim.x) {
+    const int x = k / (g.ny + 1), y = k % (g.ny + 1);
+    const double2 v = f[g.idx(x, y)];
+    fd[2 * k] = v.x;
+    fd[2 * k + 1] = v.y;
+  }
+  __syncthreads();
+  const int node = blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= n / 2) return;
+  double s0 = 0.0, s1 = 0.0;
+  for (int k = 0; k < n; ++k) {
+    const double fk = fd[k];
+    s0 = fma(Ainv[static_cast<long>(k) * n + 2 * node], fk, s0);
+    s1 = fma(Ainv[static_cast<long>(k) * n + 2 * node + 1], fk, s1);
+  }
+  const int x = node / (g.ny + 1), y = node % (g.ny + 1);
+  u[g.idx(x, y)] = make_double2(s0, s1);
+}
+
+// --------------------------------------------------- PCG vector ops (K8) --
+
+// Grid-stride dot over flat padded vectors (ghosts are 0 and add exactly 0).
+__global__ void __launch_bounds__(kRedThreads) k_dot(const double2* __restrict__ a,
+                                                     const double2* __restrict__ b, long n2,
+                                                     double* partials, unsigned* ticket, RedOp op,
+                                                     PcgState* st, HostMirror* hm, double* out) {
+  double s = 0.0;
+  for (long k = blockIdx.x * static_cast<long>(kRedThreads) + threadIdx.x; k < n2;
+       k += static_cast<long>(gridDim.x) * kRedThreads) {
+    const double2 u = a[k], v = b[k];
+    s = fma(u.x, v.x, s);
+    s = fma(u.y, v.y, s);
+  }
+  finish_reduction<kRedThreads>(s, partials, ticket, gridDim.x, op, st, hm, out);
+}
+
+// p = z + beta p (solvers.cpp:367-371); beta = 0 on the first iteration.
+__global__ void __launch_bounds__(kRedThreads) k_update_p(const double2* __restrict__ z,
+                                                          double2* __restrict__ p, long n2,
+                                                          const PcgState* st) {
+  const double beta = st->beta;
+  for (long k = blockIdx.x * static_cast<long>(kRedThreads) + threadIdx.x; k < n2;
+       k += static_cast<long>(gridDim.x) * kRedThreads) {
+    const double2 zz = z[k], pp = p[k];
+    p[k] = make_double2(zz.x + beta * pp.x, zz.y + beta * pp.y);
+  }
+}
+
+// x += alpha p; r -= alpha Ap; rr = r.r (solvers.cpp:383-386)
+__global__ void __launch_bounds__(kRedThreads) k_update_xr(double2* __restrict__ x,
+                                                           double2* __restrict__ r,
+                                                           const double2* __restrict__ p,
+                                                           const double2* __restrict__ ap, long n2,
+                                                           double* partials, unsigned* ticket,
+                                                           PcgState* st, HostMirror* hm) {
+  const double alpha = st->alpha;
+  double s = 0.0;
+  for (long k = blockIdx.x * static_cast<long>(kRedThreads) + threadIdx.x; k < n2;
+       k += static_cast<long>(gridDim.x) * kRedThreads) {
+    const double2 pp = p[k], aa = ap[k];
+    double2 xx = x[k], rr = r[k];
+    xx.x += alpha * pp.x;
+    xx.y += alpha * pp.y;
+    rr.x += -alpha * aa.x;
+    rr.y += -alpha * aa.y;
+    x[k] = xx;
+    r[k] = rr;
+    s = fma(rr.x, rr.x, s);
+    s = fma(rr.y, rr.y, s);
+  }
+  finish_reduction<kRedThreads>(s, partials, ticket, gridDim.x, kRedRr, st, hm, nullptr);
+}
+
+// r = b - t (t = A x0) ; plain copy when t == nullptr
+__global__ void k_sub(const double2* __restrict__ b, const double2* __restrict__ t,
+                      double2* __restrict__ r, long n2) {
+  for (long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; k < n2;
+       k += static_cast<long>(gridDim.x) * blockDim.x) {
+    const double2 bb = b[k];
+    if (t) {
+      const double2 tt = t[k];
+      r[k] = make_double2(bb.x - tt.x, bb.y - tt.y);
+    } else {
+      r[k] = bb;
+    }
+  }
+}
+
+__global__ void k_pcg_begin(PcgState* st) {
+  st->it = 1;
+  st->status = 0;
+  st->zr_prev = 0.0;
+  st->beta = 0.0;
+}
+
+// ------------------------------------------------------ consumers (K9-K11)
+
+// u_e^T khat u_e (fem.cpp:292-318), unmasked u, dense element-major output.
+__global__ void k_element_energy(Grid g, const double2* __restrict__ u, double* __restrict__ out) {
+  const int ey = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ex = blockIdx.y;
+  if (ey >= g.ny) return;
+  const long i = g.idx(ex, ey);
+  double ue[8];
+  const double2 a = u[i], b = u[i + g.P], c = u[i + g.P + 1], d = u[i + 1];
+  ue[0] = a.x; ue[1] = a.y; ue[2] = b.x; ue[3] = b.y;
+  ue[4] = c.x; ue[5] = c.y; ue[6] = d.x; ue[7] = d.y;
+  double s = 0.0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    double row = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) row = fma(c_ke[r * 8 + q], ue[q], row);
+    s = fma(ue[r], row, s);
+  }
+  out[static_cast<long>(ex) * g.ny + ey] = s;
+}
+
+// -p alpha^(p-1) E0 * energy for every phase (mto.cpp:61-85)
+__global__ void k_sensitivity(long ne, int np, const double* __restrict__ alpha,
+                              const double* __restrict__ energy, const double* __restrict__ pm,
+                              double pen, double* __restrict__ out) {
+  for (long e = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; e < ne;
+       e += static_cast<long>(gridDim.x) * blockDim.x) {
+    const double en = energy[e];
+    for (int i = 0; i < np; ++i) {
+      const double a = alpha[e * np + i];
+      const double pw1 = (pen == 3.0) ? a * a : pow(a, pen - 1.0);
+      out[i * ne + e] = -pen * pw1 * pm[i] * en;
+    }
+  }
+}
+
+// E_e = sum_i alpha_i^p E_i (density.cpp:68-85) into the padded modulus grid
+__global__ void k_simp(Grid g, int np, const double* __restrict__ alpha,
+                       const double* __restrict__ pm, double pen, double* __restrict__ E) {
+  const int ey = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ex = blockIdx.y;
+  if (ey >= g.ny) return;
+  const long e = static_cast<long>(ex) * g.ny + ey;
+  double v = 0.0;
+  for (int i = 0; i < np; ++i) {
+    const double a = alpha[e * np + i];
+    const double ap = (pen == 3.0) ? a * a * a : pow(a, pen);
+    v += ap * pm[i];
+  }
+  E[g.idx(ex, ey)] = v;
+}
+
+// density-weighted cone sensitivity filter (mto.cpp:87-117)
+__global__ void k_filter(int nx, int ny, int np, int phase, double radius, int reach,
+                         const double* __restrict__ alpha, const double* __restrict__ raw,
+                         double* __restrict__ out) {
+  const int ey = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ex = blockIdx.y;
+  if (ey >= ny) return;
+  double acc = 0.0, ws = 0.0;
+  const int x0 = max(0, ex - reach), x1 = min(nx - 1, ex + reach);
+  const int y0 = max(0, ey - reach), y1 = min(ny - 1, ey + reach);
+  for (int jx = x0; jx <= x1; ++jx)
+    for (int jy = y0; jy <= y1; ++jy) {
+      const double w = radius - sqrt(static_cast<double>((ex - jx) * (ex - jx) + (ey - jy) * (ey - jy)));
+      if (w <= 0.0) continue;
+      const long j = static_cast<long>(jx) * ny + jy;
+      acc += w * alpha[j * np + phase] * raw[j];
+      ws += w;
+    }
+  const long e = static_cast<long>(ex) * ny + ey;
+  out[e] = acc / (alpha[e * np + phase] * ws);
+}
+
+}  // namespace tmg

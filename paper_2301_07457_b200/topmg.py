@@ -1,0 +1,433 @@
+"""Python mirror of the reference topopt-mg interface for the pCGMG hot path.
+
+Names, argument meaning and error types follow the reference so that code and
+tests written against it read the same (citations: /root/reference/proj):
+
+  GridLevel, BoundaryConditions       grid.hpp:10-24, fem.hpp:14-19
+  SolverConfig, SolveReport           solvers.hpp:17-37
+  element_stiffness                   fem.cpp:131-169
+  effective_moduli                    density.cpp:78-85
+  wall_boundary_conditions            fem.cpp:320-336
+  build_multigrid_operators           solvers.cpp:460-481  (GPU: matrix-free)
+  pcgmg_solve                         solvers.cpp:516-530
+  mg_cycle                            solvers.cpp:483-514
+  compliance / element_energies       fem.cpp:284-318
+  sensitivities / filter_sensitivities mto.cpp:61-117
+  ConfigError ... MultiplierError     errors.hpp:9-47
+
+Everything that computes runs in libtmg_gpu.so on an sm_100 GPU; this module
+only marshals arrays. There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import dptr, iptr
+
+
+# ----------------------------------------------------------------- errors --
+class TopmgError(RuntimeError):
+    pass
+
+
+class ConfigError(TopmgError):
+    pass
+
+
+class DimensionError(TopmgError):
+    pass
+
+
+class NumericError(TopmgError):
+    pass
+
+
+class DefinitenessError(NumericError):
+    def __init__(self, what: str, row: int = -1):
+        super().__init__(what)
+        self.row = row
+
+
+class SplittingError(NumericError):
+    pass
+
+
+class PreconditionerError(NumericError):
+    pass
+
+
+class MultiplierError(NumericError):
+    pass
+
+
+class CudaError(TopmgError):
+    pass
+
+
+def _raise(code: int, msg: str, row: int = -1):
+    if code == 1:
+        raise ConfigError(msg)
+    if code == 2:
+        raise DimensionError(msg)
+    if code == 3:
+        raise DefinitenessError(msg, row)
+    if code == 4:
+        raise PreconditionerError(msg)
+    if code == 5:
+        raise SplittingError(msg)
+    if code == 8:
+        raise MultiplierError(msg)
+    raise CudaError(msg or f"tmg_gpu status {code}")
+
+
+# ------------------------------------------------------------------ types --
+@dataclass
+class GridLevel:
+    nx: int = 0
+    ny: int = 0
+    dofs_per_node: int = 2
+    level_index: int = 0
+
+    def node_count(self) -> int:
+        return (self.nx + 1) * (self.ny + 1)
+
+    def dof_count(self) -> int:
+        return self.dofs_per_node * self.node_count()
+
+    def element_count(self) -> int:
+        return self.nx * self.ny
+
+    def node_index(self, x: int, y: int) -> int:
+        return x * (self.ny + 1) + y
+
+    def dof_index(self, x: int, y: int, c: int) -> int:
+        return self.node_index(x, y) * self.dofs_per_node + c
+
+    def element_index(self, ex: int, ey: int) -> int:
+        return ex * self.ny + ey
+
+
+@dataclass
+class BoundaryConditions:
+    fixed_dofs: list = field(default_factory=list)
+    point_loads: list = field(default_factory=list)  # (dof, value)
+
+
+@dataclass
+class SolverConfig:
+    method: str = "pcgmg"
+    tol: float = 1e-6
+    max_iter: int = 1000
+    omega: float = 0.6
+    gamma: int = 1
+    pre_sweeps: int = 2
+    post_sweeps: int = 2
+    num_coarsenings: int = 2
+
+    def validate(self):
+        """SolverConfig::validate (solvers.cpp:72-88)."""
+        if not self.tol > 0.0:
+            raise ConfigError("solver tol must be positive")
+        if self.max_iter < 1:
+            raise ConfigError("max_iter must be >= 1")
+        if not (0.0 < self.omega <= 1.0):
+            raise ConfigError(f"omega must lie in (0, 1], got {self.omega:f}")
+        if self.gamma not in (1, 2):
+            raise ConfigError("gamma must be 1 (V-cycle) or 2 (W-cycle)")
+        if self.pre_sweeps < 0 or self.post_sweeps < 0:
+            raise ConfigError("smoothing sweep counts must be non-negative")
+        if self.num_coarsenings < 0:
+            raise ConfigError("num_coarsenings must be non-negative")
+        if self.method == "pcgmg" and self.pre_sweeps != self.post_sweeps:
+            raise ConfigError("pcgmg needs pre_sweeps == post_sweeps for a symmetric preconditioner")
+
+
+@dataclass
+class SolveReport:
+    solution: np.ndarray = None
+    iterations: int = 0
+    final_residual: float = 0.0
+    converged: bool = False
+    seconds: float = 0.0
+    residual_history: list = field(default_factory=list)
+
+
+@dataclass
+class MaterialModel:
+    phase_moduli: list = field(default_factory=lambda: [1.0, 0.5, 0.2, 1e-9])
+    poisson_ratio: float = 0.3
+    penalty: float = 3.0
+
+    def num_phases(self) -> int:
+        return len(self.phase_moduli)
+
+
+# --------------------------------------------------------- host producers --
+def element_stiffness(modulus: float, poisson_ratio: float) -> np.ndarray:
+    """8x8 Q4 plane-stress Ke (fem.cpp:131-169), row-major."""
+    k = np.zeros(64)
+    _lib.load().tmg_element_stiffness(modulus, poisson_ratio, dptr(k))
+    return k.reshape(8, 8)
+
+
+def effective_moduli(alpha: np.ndarray, material: MaterialModel) -> np.ndarray:
+    """E_e = sum_i alpha_i^p E_i (density.cpp:68-85); alpha is [ne, nphases]."""
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    ne, npn = a.shape
+    pm = np.ascontiguousarray(material.phase_moduli, dtype=np.float64)
+    out = np.empty(ne)
+    _lib.load().tmg_inputs_effective_moduli(ne, npn, dptr(a), dptr(pm), material.penalty, dptr(out))
+    return out
+
+
+def density_iid(nx: int, ny: int, seed: int, nmat: int = 3) -> np.ndarray:
+    a = np.empty((nx * ny, nmat + 1))
+    _lib.load().tmg_inputs_density_iid(nx, ny, nmat, seed, dptr(a))
+    return a
+
+
+def density_checker(nx: int, ny: int, block: int, seed: int, nphases: int = 4) -> np.ndarray:
+    a = np.empty((nx * ny, nphases))
+    _lib.load().tmg_inputs_density_checker(nx, ny, block, nphases, seed, dptr(a))
+    return a
+
+
+def wall_boundary_conditions(grid: GridLevel, load: str = "point") -> BoundaryConditions:
+    """Bottom edge clamped (fem.cpp:320-336). load='point' is the reference's
+    unit load at the top-mid node; load='uniform' is BASELINE's unit total
+    load spread as -1/(nx+1) over every top node."""
+    if load == "point" and grid.nx % 2:
+        raise ConfigError("wall load sits on the top-edge midpoint; nx must be even")
+    nx, ny = grid.nx, grid.ny
+    fixed = np.empty(2 * (nx + 1), np.int32)
+    nf = C.c_int()
+    ld = np.empty(nx + 1, np.int32)
+    lv = np.empty(nx + 1)
+    nl = C.c_int()
+    _lib.load().tmg_inputs_wall_bc(nx, ny, 0 if load == "point" else 1, iptr(fixed), C.byref(nf),
+                                   iptr(ld), dptr(lv), C.byref(nl))
+    return BoundaryConditions(fixed_dofs=fixed[: nf.value].tolist(),
+                              point_loads=list(zip(ld[: nl.value].tolist(), lv[: nl.value].tolist())))
+
+
+def assemble_rhs(grid: GridLevel, bc: BoundaryConditions) -> np.ndarray:
+    """rhs of assemble_from_moduli: loads summed, fixed entries zeroed."""
+    fixed = np.ascontiguousarray(bc.fixed_dofs, dtype=np.int32)
+    ld = np.ascontiguousarray([d for d, _ in bc.point_loads], dtype=np.int32)
+    lv = np.ascontiguousarray([v for _, v in bc.point_loads], dtype=np.float64)
+    b = np.empty(grid.dof_count())
+    _lib.load().tmg_inputs_rhs(grid.nx, grid.ny, iptr(fixed), len(fixed), iptr(ld), dptr(lv), len(lv), dptr(b))
+    return b
+
+
+# ------------------------------------------------------------- GPU solver --
+class MultigridOperators:
+    """GPU-resident counterpart of MultigridOperators (solvers.hpp:93-102).
+
+    Holds the matrix-free fine operator (moduli, Ke, Dirichlet mask), the
+    device Galerkin hierarchy and the coarsest inverse; rebuilt by
+    ``set_moduli`` each outer iteration while the mesh stays resident.
+    """
+
+    def __init__(self, grid: GridLevel, num_coarsenings: int, poisson_ratio: float,
+                 bc: BoundaryConditions, device: int = 0):
+        self.lib = _lib.load()
+        self.grid = grid
+        self.num_coarsenings = num_coarsenings
+        self.omega = 0.6
+        h = C.c_void_p()
+        st = self.lib.tmg_gpu_create(grid.nx, grid.ny, num_coarsenings, grid.dofs_per_node, device,
+                                     C.byref(h))
+        self.h = h
+        if st != 0:
+            msg, row = self._err()
+            self.close()
+            _raise(st, msg, row)
+        fixed = np.ascontiguousarray(bc.fixed_dofs, dtype=np.int32)
+        self._check(self.lib.tmg_gpu_set_problem(self.h, poisson_ratio, iptr(fixed), len(fixed)))
+
+    # ---- plumbing
+    def _err(self):
+        buf = C.create_string_buffer(512)
+        row = C.c_int(-1)
+        if self.h:
+            self.lib.tmg_gpu_last_error(self.h, buf, 512, C.byref(row))
+        return buf.value.decode(errors="replace"), row.value
+
+    def _check(self, st: int):
+        if st != 0:
+            msg, row = self._err()
+            _raise(st, msg, row)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.tmg_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return self.lib.tmg_gpu_stream(self.h) or 0
+
+    def launch_count(self) -> int:
+        return self.lib.tmg_gpu_launch_count(self.h)
+
+    def level(self, index: int) -> GridLevel:
+        s = 1 << (self.num_coarsenings - index)
+        return GridLevel(self.grid.nx // s, self.grid.ny // s, 2, index)
+
+    # ---- setup (assemble_elasticity + build_multigrid_operators)
+    def set_moduli(self, moduli: np.ndarray, omega: float = 0.6):
+        e = np.ascontiguousarray(moduli, dtype=np.float64)
+        self.omega = omega
+        self._check(self.lib.tmg_gpu_set_moduli(self.h, dptr(e), e.size, omega))
+
+    def upload_moduli(self, moduli: np.ndarray):
+        e = np.ascontiguousarray(moduli, dtype=np.float64)
+        self._check(self.lib.tmg_gpu_upload_moduli(self.h, dptr(e), e.size))
+
+    def setup(self, omega: float = 0.6):
+        self.omega = omega
+        self._check(self.lib.tmg_gpu_setup(self.h, omega))
+
+    def set_density(self, alpha: np.ndarray, material: MaterialModel, omega: float = 0.6):
+        a = np.ascontiguousarray(alpha, dtype=np.float64)
+        pm = np.ascontiguousarray(material.phase_moduli, dtype=np.float64)
+        self.omega = omega
+        self._check(self.lib.tmg_gpu_set_density(self.h, dptr(a), a.shape[1], dptr(pm), material.penalty, omega))
+
+    # ---- kernel-level entry points
+    def apply(self, level: int, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty_like(x)
+        self._check(self.lib.tmg_gpu_apply(self.h, level, dptr(x), dptr(y)))
+        return y
+
+    def level_values(self, level: int, offsets: np.ndarray, cols: np.ndarray) -> np.ndarray:
+        off = np.ascontiguousarray(offsets, dtype=np.int32)
+        col = np.ascontiguousarray(cols, dtype=np.int32)
+        vals = np.empty(len(col))
+        self._check(self.lib.tmg_gpu_level_values(self.h, level, iptr(off), iptr(col), dptr(vals)))
+        return vals
+
+    def prolongate(self, level: int, coarse: np.ndarray) -> np.ndarray:
+        c = np.ascontiguousarray(coarse, dtype=np.float64)
+        out = np.empty(self.level(level).dof_count())
+        self._check(self.lib.tmg_gpu_prolongate(self.h, level, dptr(c), dptr(out)))
+        return out
+
+    def restrict(self, level: int, fine: np.ndarray) -> np.ndarray:
+        f = np.ascontiguousarray(fine, dtype=np.float64)
+        out = np.empty(self.level(level - 1).dof_count())
+        self._check(self.lib.tmg_gpu_restrict(self.h, level, dptr(f), dptr(out)))
+        return out
+
+    def smooth(self, level: int, f: np.ndarray, u: np.ndarray, sweeps: int) -> np.ndarray:
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        u = np.array(u, dtype=np.float64, copy=True)
+        self._check(self.lib.tmg_gpu_smooth(self.h, level, dptr(f), dptr(u), sweeps))
+        return u
+
+    def time_kernel(self, which: int, reps: int):
+        ms = C.c_double()
+        by = C.c_double()
+        self._check(self.lib.tmg_gpu_time_kernel(self.h, which, reps, C.byref(ms), C.byref(by)))
+        return ms.value, by.value
+
+    def last_timings(self):
+        s = C.c_double()
+        p = C.c_double()
+        self.lib.tmg_gpu_last_timings(self.h, C.byref(s), C.byref(p))
+        return s.value, p.value
+
+
+def build_multigrid_operators(grid: GridLevel, moduli: np.ndarray, poisson_ratio: float,
+                              bc: BoundaryConditions, num_coarsenings: int, omega: float = 0.6,
+                              device: int = 0) -> MultigridOperators:
+    """assemble_from_moduli + build_hierarchy + build_multigrid_operators
+    (fem.cpp:181, grid.cpp:53, solvers.cpp:460) as one device setup."""
+    ops = MultigridOperators(grid, num_coarsenings, poisson_ratio, bc, device)
+    ops.set_moduli(moduli, omega)
+    return ops
+
+
+def mg_cycle(ops: MultigridOperators, u: np.ndarray, f: np.ndarray, gamma: int = 1,
+             pre_sweeps: int = 2, post_sweeps: int = 2) -> np.ndarray:
+    """One gamma-cycle at the finest level (solvers.cpp:483-514); returns u."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    u = np.array(u, dtype=np.float64, copy=True)
+    ops._check(ops.lib.tmg_gpu_vcycle(ops.h, dptr(f), dptr(u), gamma, pre_sweeps, post_sweeps))
+    return u
+
+
+def pcgmg_solve(ops: MultigridOperators, b: np.ndarray, cfg: SolverConfig,
+                x0: np.ndarray | None = None) -> SolveReport:
+    """pcgmg_solve (solvers.cpp:516-530): PCG with one gamma-cycle as M^-1."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if b.size != ops.grid.dof_count():
+        raise DimensionError(f"rhs length {b.size} != dof count {ops.grid.dof_count()}")
+    x0c = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+    x = np.empty_like(b)
+    it = C.c_int()
+    fr = C.c_double()
+    cv = C.c_int()
+    sec = C.c_double()
+    hist = np.empty(cfg.max_iter + 1)
+    hl = C.c_int()
+    ops._check(ops.lib.tmg_gpu_solve(ops.h, dptr(b), dptr(x0c), cfg.tol, cfg.max_iter, cfg.gamma,
+                                     cfg.pre_sweeps, cfg.post_sweeps, dptr(x), C.byref(it), C.byref(fr),
+                                     C.byref(cv), C.byref(sec), dptr(hist), hist.size, C.byref(hl)))
+    return SolveReport(solution=x, iterations=it.value, final_residual=fr.value, converged=bool(cv.value),
+                       seconds=sec.value, residual_history=hist[: hl.value].tolist())
+
+
+def compliance(ops: MultigridOperators, u: np.ndarray | None = None) -> float:
+    """u^T K u (fem.cpp:284-290); u=None uses the resident solution."""
+    uc = None if u is None else np.ascontiguousarray(u, dtype=np.float64)
+    out = C.c_double()
+    ops._check(ops.lib.tmg_gpu_compliance(ops.h, dptr(uc), C.byref(out)))
+    return out.value
+
+
+def element_energies(ops: MultigridOperators, u: np.ndarray | None = None) -> np.ndarray:
+    uc = None if u is None else np.ascontiguousarray(u, dtype=np.float64)
+    out = np.empty(ops.grid.element_count())
+    ops._check(ops.lib.tmg_gpu_element_energies(ops.h, dptr(uc), dptr(out)))
+    return out
+
+
+def sensitivities(ops: MultigridOperators, alpha: np.ndarray, material: MaterialModel,
+                  u: np.ndarray | None = None) -> np.ndarray:
+    """[nphases, ne] dC/dalpha (mto.cpp:61-85)."""
+    uc = None if u is None else np.ascontiguousarray(u, dtype=np.float64)
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    pm = np.ascontiguousarray(material.phase_moduli, dtype=np.float64)
+    out = np.empty((a.shape[1], a.shape[0]))
+    ops._check(ops.lib.tmg_gpu_sensitivities(ops.h, dptr(uc), a.shape[1], dptr(a), dptr(pm),
+                                             material.penalty, dptr(out)))
+    return out
+
+
+def filter_sensitivities(ops: MultigridOperators, raw: np.ndarray, alpha: np.ndarray, phase: int,
+                         radius: float) -> np.ndarray:
+    """Density-weighted cone sensitivity filter (mto.cpp:87-117)."""
+    r = np.ascontiguousarray(raw, dtype=np.float64)
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    if r.size != ops.grid.element_count():
+        raise DimensionError("filter: field length does not match element count")
+    out = np.empty_like(r)
+    ops._check(ops.lib.tmg_gpu_filter(ops.h, a.shape[1], dptr(a), phase, radius, dptr(r), dptr(out)))
+    return out
+
+
+__all__ = [n for n in dir() if not n.startswith("_") and n not in ("C", "dataclasses", "np", "dataclass", "field")]

@@ -1,0 +1,273 @@
+"""GPU pCGMG vs the CPU checker on identical seeded inputs.
+
+Bars (north star): relative L2 error of u <= 1e-8, compliance within 1e-9
+relative, PCG iteration count within +-2. Kernel-level pins are tighter:
+operator / Galerkin entries <= 1e-13 relative to the largest entry, one
+V-cycle <= 1e-12 relative. The checker is oracle/liboracle.so, itself pinned
+bit-for-bit to the reference (tests/test_oracle_pin.py).
+"""
+import numpy as np
+import pytest
+
+import paper_2301_07457_b200 as P
+from helpers import MAT, pair, rel
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [(8, 8, 2), (16, 16, 3), (32, 16, 2), (24, 40, 3), (64, 64, 3), (128, 128, 4)]
+
+
+@pytest.mark.parametrize("nx,ny,nc", SIZES)
+def test_fine_apply_matches_assembled_matvec(nx, ny, nc):
+    ops, sysc, b, _, _ = pair(nx, ny, nc)
+    x = np.random.default_rng(3).standard_normal(sysc.n)
+    y = ops.apply(nc, x)
+    yr = sysc.matvec(nc, x)
+    assert np.max(np.abs(y - yr)) <= 1e-13 * np.max(np.abs(yr))
+
+
+@pytest.mark.parametrize("nx,ny,nc", SIZES)
+def test_galerkin_hierarchy_matches_reference_entries(nx, ny, nc):
+    ops, sysc, b, _, _ = pair(nx, ny, nc)
+    for lvl in range(nc + 1):
+        off, col, val = sysc.csr(lvl)
+        got = ops.level_values(lvl, off, col)
+        scale = np.max(np.abs(val))
+        assert np.max(np.abs(got - val)) <= 1e-13 * scale, f"level {lvl}"
+
+
+@pytest.mark.parametrize("nx,ny,nc", SIZES)
+def test_coarse_level_apply(nx, ny, nc):
+    ops, sysc, b, _, _ = pair(nx, ny, nc)
+    rng = np.random.default_rng(4)
+    for lvl in range(nc):
+        x = rng.standard_normal(sysc.csr(lvl)[0].size - 1)
+        y = ops.apply(lvl, x)
+        yr = sysc.matvec(lvl, x)
+        assert np.max(np.abs(y - yr)) <= 1e-13 * np.max(np.abs(yr)), f"level {lvl}"
+
+
+@pytest.mark.parametrize("nx,ny,nc", [(16, 16, 3), (64, 32, 3)])
+def test_jacobi_sweeps_match_csr_formula(nx, ny, nc):
+    ops, sysc, b, _, _ = pair(nx, ny, nc)
+    rng = np.random.default_rng(5)
+    for lvl in range(1, nc + 1):
+        off, col, val = sysc.csr(lvl)
+        n = off.size - 1
+        diag = np.array([val[off[i]:off[i + 1]][col[off[i]:off[i + 1]] == i][0] for i in range(n)])
+        f = rng.standard_normal(n)
+        u = rng.standard_normal(n)
+        want = u.copy()
+        for _ in range(2):
+            want = want + 0.6 * (f - sysc.matvec(lvl, want)) / diag
+        got = ops.smooth(lvl, f, u, 2)
+        assert rel(got, want) <= 1e-13
+
+
+@pytest.mark.parametrize("nx,ny,nc", SIZES)
+@pytest.mark.parametrize("gamma", [1, 2])
+def test_one_cycle_matches_mg_cycle(nx, ny, nc, gamma):
+    ops, sysc, b, _, _ = pair(nx, ny, nc)
+    rng = np.random.default_rng(6)
+    f = rng.standard_normal(sysc.n)
+    for u0 in (np.zeros(sysc.n), rng.standard_normal(sysc.n)):
+        got = P.mg_cycle(ops, u0, f, gamma, 2, 2)
+        want = sysc.vcycle(f, u0, gamma, 2, 2)
+        assert rel(got, want) <= 1e-12
+
+
+def test_transfer_properties():
+    """test_grid.cpp:106-155 restated for the device transfer kernels."""
+    ops, sysc, b, _, _ = pair(16, 16, 2)
+    fine = ops.level(2)
+    coarse = ops.level(1)
+    # prolongation reproduces linear fields exactly (test_grid.cpp:53-104)
+    xs = np.array([[x, y] for x in range(coarse.nx + 1) for y in range(coarse.ny + 1)], float)
+    uc = np.stack([2 * xs[:, 0] + 3 * xs[:, 1], -xs[:, 0] + 0.5 * xs[:, 1]], 1).ravel()
+    uf = ops.prolongate(2, uc)
+    xf = np.array([[x, y] for x in range(fine.nx + 1) for y in range(fine.ny + 1)], float) / 2
+    want = np.stack([2 * xf[:, 0] + 3 * xf[:, 1], -xf[:, 0] + 0.5 * xf[:, 1]], 1).ravel()
+    assert np.max(np.abs(uf - want)) < 1e-13
+    # variational pairing <P u, v> = <u, 4 R v> (test_grid.cpp:140-155)
+    rng = np.random.default_rng(7)
+    u = rng.standard_normal(coarse.dof_count())
+    v = rng.standard_normal(fine.dof_count())
+    lhs = np.dot(ops.prolongate(2, u), v)
+    rhs = np.dot(u, 4 * ops.restrict(2, v))
+    assert abs(lhs - rhs) <= 1e-12 * max(1.0, abs(lhs))
+    # interior coarse node of restricted ones = 1 (test_grid.cpp:106-120)
+    rc = ops.restrict(2, np.ones(fine.dof_count()))
+    k = coarse.node_index(3, 4)
+    assert abs(rc[2 * k] - 1.0) < 1e-15 and abs(rc[2 * k + 1] - 1.0) < 1e-15
+
+
+CASES = [
+    (16, 16, 2, "iid", 0, "uniform"),
+    (32, 32, 3, "iid", 1, "point"),
+    (64, 64, 3, "uniform", 0, "uniform"),  # config 0 initial design
+    (64, 64, 3, "checker", 2, "uniform"),
+    (128, 64, 4, "iid", 3, "uniform"),
+    (256, 256, 5, "iid", 0, "uniform"),
+]
+
+
+@pytest.mark.parametrize("nx,ny,nc,recipe,seed,load", CASES)
+def test_pcgmg_solve_parity(nx, ny, nc, recipe, seed, load):
+    ops, sysc, b, _, _ = pair(nx, ny, nc, recipe, seed, load)
+    cfg = P.SolverConfig(tol=1e-8, max_iter=2000, num_coarsenings=nc)
+    rep = P.pcgmg_solve(ops, b, cfg)
+    ref = sysc.solve(b, tol=1e-8, max_iter=2000)
+    assert rep.converged and ref["converged"]
+    assert abs(rep.iterations - ref["iterations"]) <= 2
+    assert rel(rep.solution, ref["solution"]) <= 1e-8
+    c_gpu = P.compliance(ops)
+    c_ref = sysc.compliance(ref["solution"])
+    assert abs(c_gpu - c_ref) <= 1e-9 * abs(c_ref)
+    assert len(rep.residual_history) == rep.iterations + 1
+    assert rep.residual_history[-1] == rep.final_residual <= 1e-8
+    # relative residual of the GPU solution under the reference's assembled K
+    r = b - sysc.matvec(nc, rep.solution)
+    assert np.linalg.norm(r) / np.linalg.norm(b) <= 1e-8 * 1.0001
+
+
+def test_reference_itself_when_available():
+    if not po.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    ops, sysc, b, _, _ = pair(64, 64, 3, kind="ref")
+    rep = P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-8, max_iter=500))
+    ref = sysc.solve(b, tol=1e-8, max_iter=500)
+    assert abs(rep.iterations - ref["iterations"]) <= 2
+    assert rel(rep.solution, ref["solution"]) <= 1e-8
+
+
+def test_tight_tolerance_matches_direct_solution():
+    """acceptance.cpp:156-190: pCGMG at tol 1e-10 within 1e-8 of Cholesky."""
+    ops, sysc, b, _, _ = pair(32, 32, 2, recipe="uniform")
+    rep = P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-10, max_iter=2000))
+    tight = sysc.solve(b, tol=1e-14, max_iter=5000)
+    assert rel(rep.solution, tight["solution"]) <= 1e-8
+
+
+def test_warm_start_and_zero_rhs_and_max_iter():
+    ops, sysc, b, _, _ = pair(32, 32, 3)
+    cfg = P.SolverConfig(tol=1e-8, max_iter=500)
+    first = P.pcgmg_solve(ops, b, cfg)
+    ref = sysc.solve(b, tol=1e-8, max_iter=500, x0=first.solution * 0.99)
+    warm = P.pcgmg_solve(ops, b, cfg, x0=first.solution * 0.99)
+    assert abs(warm.iterations - ref["iterations"]) <= 2
+    assert rel(warm.solution, ref["solution"]) <= 1e-8
+    # already converged warm start: 0 iterations (solvers.cpp:351-357)
+    done = P.pcgmg_solve(ops, b, cfg, x0=first.solution)
+    assert done.converged and done.iterations == 0 and len(done.residual_history) == 1
+    # zero rhs: zero solution, converged, history {0} (solvers.cpp:338-344)
+    z = P.pcgmg_solve(ops, np.zeros_like(b), cfg, x0=first.solution)
+    assert z.converged and z.iterations == 0 and z.residual_history == [0.0]
+    assert not np.any(z.solution)
+    # max_iter exhausted: not converged, not an error
+    short = P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-14, max_iter=3))
+    rs = sysc.solve(b, tol=1e-14, max_iter=3)
+    assert not short.converged and short.iterations == 3
+    assert rel(short.solution, rs["solution"]) <= 1e-10
+
+
+def test_single_level_hierarchy_solves_in_one_iteration():
+    """test_solvers.cpp:328-342 for the elasticity system."""
+    ops, sysc, b, _, _ = pair(8, 8, 0)
+    rep = P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-6))
+    assert rep.converged and rep.iterations == 1
+    ref = sysc.solve(b, tol=1e-6)
+    assert rel(rep.solution, ref["solution"]) <= 1e-12
+
+
+def test_errors_mirror_reference():
+    g = P.GridLevel(10, 8)
+    with pytest.raises(P.ConfigError):
+        P.MultigridOperators(g, 2, 0.3, P.wall_boundary_conditions(g, "uniform"))
+    ops, sysc, b, _, _ = pair(16, 16, 2)
+    with pytest.raises(P.ConfigError):
+        P.pcgmg_solve(ops, b, P.SolverConfig(pre_sweeps=2, post_sweeps=3))
+    with pytest.raises(P.DimensionError):
+        ops.set_moduli(np.ones(5))
+    with pytest.raises(P.ConfigError):
+        P.MultigridOperators(P.GridLevel(8, 8), 1, 0.3, P.BoundaryConditions([1000], []))
+    # unconstrained structure: singular coarsest operator (solvers.cpp:144-148)
+    free = P.MultigridOperators(P.GridLevel(8, 8), 2, 0.3, P.BoundaryConditions([], []))
+    with pytest.raises(P.DefinitenessError):
+        free.set_moduli(np.ones(64))
+
+
+def test_duplicate_fixed_dofs_follow_finish_assembly():
+    g = P.GridLevel(16, 16)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    bc.fixed_dofs = bc.fixed_dofs + bc.fixed_dofs[:6]
+    ops, sysc, b, _, _ = pair(16, 16, 2, bc=bc)
+    x = np.random.default_rng(8).standard_normal(sysc.n)
+    assert np.max(np.abs(ops.apply(2, x) - sysc.matvec(2, x))) <= 1e-13 * np.max(np.abs(sysc.matvec(2, x)))
+    rep = P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-8))
+    ref = sysc.solve(b, tol=1e-8)
+    assert rel(rep.solution, ref["solution"]) <= 1e-8
+
+
+def test_preconditioner_is_symmetric():
+    """test_solvers.cpp:387-409 / acceptance criterion 6."""
+    ops, sysc, b, _, _ = pair(8, 8, 2)
+    n = sysc.n
+    m = np.zeros((n, n))
+    for j in range(n):
+        e = np.zeros(n)
+        e[j] = 1.0
+        m[:, j] = P.mg_cycle(ops, np.zeros(n), e)
+    assert np.max(np.abs(m - m.T)) < 1e-10 * max(1.0, np.max(np.abs(m)))
+
+
+def test_bitwise_determinism():
+    ops, sysc, b, _, _ = pair(64, 64, 3)
+    cfg = P.SolverConfig(tol=1e-9)
+    r1 = P.pcgmg_solve(ops, b, cfg)
+    r2 = P.pcgmg_solve(ops, b, cfg)
+    assert r1.iterations == r2.iterations
+    assert r1.residual_history == r2.residual_history
+    assert np.array_equal(r1.solution, r2.solution)
+
+
+@pytest.mark.parametrize("nx,ny", [(16, 16), (40, 24)])
+def test_consumers_match_reference(nx, ny):
+    ops, sysc, b, alpha, E = pair(nx, ny, 2)
+    rep = P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-10))
+    u = rep.solution
+    en = P.element_energies(ops)
+    en_r = po.element_energies("orc", nx, ny, u, 0.3)
+    assert np.max(np.abs(en - en_r)) <= 1e-13 * np.max(np.abs(en_r))
+    s = P.sensitivities(ops, alpha, MAT)
+    s_r = po.sensitivities("orc", nx, ny, alpha, MAT.phase_moduli, MAT.penalty, 0.3, u)
+    assert np.max(np.abs(s - s_r)) <= 1e-13 * np.max(np.abs(s_r))
+    # alpha_void can be exactly 0 in the iid recipe: the reference then divides
+    # by zero (mto.cpp:114); both sides must agree on where that happens
+    floored = np.maximum(alpha, 1e-3)
+    for a in (alpha, floored):
+        for radius in (1.0, 1.5, 3.0):
+            for ph in range(4):
+                f = P.filter_sensitivities(ops, s[ph], a, ph, radius)
+                f_r = po.filter_sensitivities("orc", nx, ny, a, ph, radius, s_r[ph])
+                fin = np.isfinite(f_r)
+                assert np.array_equal(fin, np.isfinite(f))
+                assert np.array_equal(np.isnan(f), np.isnan(f_r))
+                if fin.any():
+                    scale = np.max(np.abs(f_r[fin]))
+                    assert np.max(np.abs(f[fin] - f_r[fin])) <= 1e-12 * scale
+
+
+def test_device_simp_matches_host_moduli():
+    nx = ny = 32
+    from helpers import moduli
+    alpha, E = moduli(nx, ny, "iid", 4)
+    g = P.GridLevel(nx, ny)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    a = P.MultigridOperators(g, 3, 0.3, bc)
+    a.set_density(alpha, MAT)
+    b_ = P.MultigridOperators(g, 3, 0.3, bc)
+    b_.set_moduli(E)
+    x = np.random.default_rng(9).standard_normal(g.dof_count())
+    ya, yb = a.apply(3, x), b_.apply(3, x)
+    assert np.max(np.abs(ya - yb)) <= 1e-14 * np.max(np.abs(yb))
