@@ -174,6 +174,13 @@ int tmg_gpu_time_kernel(tmg_gpu_handle* h, int which, int reps, double* avg_ms,
                         double* bytes);
 /* Breakdown of the last resident solve: setup ms, pcg ms (device events). */
 int tmg_gpu_last_timings(tmg_gpu_handle* h, double* setup_ms, double* pcg_ms);
+/* CUDA events on the handle's stream (slots 0..7) for callers that time a
+ * region of library calls on the launching stream. */
+int tmg_gpu_event_record(tmg_gpu_handle* h, int slot);
+int tmg_gpu_event_elapsed(tmg_gpu_handle* h, int slot_a, int slot_b, double* ms);
+/* Page-locked host buffers for host<->device copies at full PCIe/C2C rate. */
+void* tmg_host_alloc(unsigned long bytes);
+void tmg_host_free(void* p);
 
 /* ---- host-side input producers (tmg_inputs.cpp) ------------------------ */
 

@@ -51,6 +51,10 @@ SIGNATURES = [
     ("tmg_gpu_launch_count", C.c_long, [_H]),
     ("tmg_gpu_time_kernel", C.c_int, [_H, C.c_int, C.c_int, _D, _D]),
     ("tmg_gpu_last_timings", C.c_int, [_H, _D, _D]),
+    ("tmg_gpu_event_record", C.c_int, [_H, C.c_int]),
+    ("tmg_gpu_event_elapsed", C.c_int, [_H, C.c_int, C.c_int, _D]),
+    ("tmg_host_alloc", C.c_void_p, [C.c_ulong]),
+    ("tmg_host_free", None, [C.c_void_p]),
     ("tmg_element_stiffness", None, [C.c_double, C.c_double, _D]),
     ("tmg_inputs_effective_moduli", None, [C.c_long, C.c_int, _D, _D, C.c_double, _D]),
     ("tmg_inputs_density_iid", None, [C.c_int, C.c_int, C.c_int, C.c_ulonglong, _D]),

@@ -114,6 +114,7 @@ struct tmg_gpu_handle {
   bool capturing = false;
   long capture_kernels = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t uev[8] = {};
   double last_setup_ms = 0.0, last_pcg_ms = 0.0;
   std::string err;
   int err_row = -1;
@@ -203,6 +204,8 @@ void free_handle(H* h) {
   if (h->hm) cudaFreeHost(h->hm);
   if (h->scal_host) cudaFreeHost(h->scal_host);
   for (cudaEvent_t e : h->ev)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->uev)
     if (e) cudaEventDestroy(e);
   if (h->stream) cudaStreamDestroy(h->stream);
 }
@@ -1036,6 +1039,35 @@ int tmg_gpu_last_timings(tmg_gpu_handle* h, double* setup_ms, double* pcg_ms) {
   if (setup_ms) *setup_ms = h->last_setup_ms;
   if (pcg_ms) *pcg_ms = h->last_pcg_ms;
   return TMG_OK;
+}
+
+int tmg_gpu_event_record(tmg_gpu_handle* h, int slot) {
+  return guarded(h, [&] {
+    if (slot < 0 || slot >= 8) fail(TMG_ERR_DIMENSION, "event slot out of range");
+    if (!h->uev[slot]) CK(cudaEventCreate(&h->uev[slot]));
+    CK(cudaEventRecord(h->uev[slot], h->stream));
+  });
+}
+
+int tmg_gpu_event_elapsed(tmg_gpu_handle* h, int a, int b, double* ms) {
+  return guarded(h, [&] {
+    if (a < 0 || a >= 8 || b < 0 || b >= 8 || !h->uev[a] || !h->uev[b])
+      fail(TMG_ERR_DIMENSION, "event slot not recorded");
+    CK(cudaEventSynchronize(h->uev[b]));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, h->uev[a], h->uev[b]));
+    *ms = f;
+  });
+}
+
+void* tmg_host_alloc(unsigned long bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void tmg_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 }  // extern "C"
