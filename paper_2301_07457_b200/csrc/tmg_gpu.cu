@@ -17,6 +17,7 @@
 
 #include "../../include/tmg_gpu.h"
 #include "tmg_kernels.cuh"
+#include "tmg_march.cuh"
 
 using namespace tmg;
 
@@ -63,7 +64,9 @@ Grid make_grid(int nx, int ny) {
   Grid g;
   g.nx = nx;
   g.ny = ny;
-  g.P = ((ny + 2 + kOY) + 7) / 8 * 8;  // y in [-1, ny+1] at offset kOY
+  // y in [-1, ny+1] at offset kOY; a multiple of 16 nodes keeps every column
+  // start 16-byte aligned for the TMA bulk copies of the byte-wide mask
+  g.P = ((ny + 2 + kOY) + 15) / 16 * 16;
   g.size = static_cast<long>(nx + 3) * g.P;
   return g;
 }
@@ -86,7 +89,8 @@ struct tmg_gpu_handle {
   double *A0 = nullptr, *LiT = nullptr, *Ainv = nullptr;
   int* bad_row = nullptr;
   // PCG (K8)
-  double2 *x = nullptr, *r = nullptr, *p = nullptr, *ap = nullptr, *b = nullptr, *x0 = nullptr;
+  double2 *x = nullptr, *r = nullptr, *ap = nullptr, *b = nullptr, *x0 = nullptr;
+  double2* pbuf[2] = {nullptr, nullptr};  // PCG directions (old / new alternate)
   double* partials = nullptr;
   unsigned* ticket = nullptr;
   PcgState* st = nullptr;
@@ -96,7 +100,7 @@ struct tmg_gpu_handle {
   double* scal_host = nullptr;   // pinned
   bool have_solution = false;
   // captured PCG iteration
-  cudaGraphExec_t graph = nullptr;
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
   int g_gamma = -1, g_pre = -1, g_post = -1;
   long graph_kernels = 0;
   double2* z_final = nullptr;
@@ -173,7 +177,8 @@ void need_setup(H* h) {
 
 void free_handle(H* h) {
   cudaSetDevice(h->device);
-  if (h->graph) cudaGraphExecDestroy(h->graph);
+  for (cudaGraphExec_t gx : h->graph)
+    if (gx) cudaGraphExecDestroy(gx);
   for (Level& L : h->lev) {
     cudaFree(L.u[0]);
     cudaFree(L.u[1]);
@@ -189,7 +194,8 @@ void free_handle(H* h) {
   cudaFree(h->bad_row);
   cudaFree(h->x);
   cudaFree(h->r);
-  cudaFree(h->p);
+  cudaFree(h->pbuf[0]);
+  cudaFree(h->pbuf[1]);
   cudaFree(h->ap);
   cudaFree(h->b);
   cudaFree(h->x0);
@@ -212,8 +218,55 @@ void free_handle(H* h) {
 
 // ------------------------------------------------------------ launches --
 
+// output columns per marching CTA: long strips amortise the prologue; short
+// ones keep small grids spread over all 148 SMs
+int march_tx(long rows_tiles, long cols) {
+  const long want = (cols * rows_tiles + 148 * 8 - 1) / (148 * 8);
+  return static_cast<int>(std::min<long>(64, std::max<long>(6, want)));
+}
+
+MarchArgs march_args(H* h, const double2* u) {
+  MarchArgs a{};
+  a.g = h->fine().g;
+  if (h->nc > 0) a.gc = h->lev[h->nc - 1].g;
+  a.u = u;
+  a.E = h->E;
+  a.M = h->M;
+  a.omega = h->omega;
+  a.partials = h->partials;
+  a.ticket = h->ticket;
+  a.rop = kRedNone;
+  a.st = h->st;
+  a.hm = h->hm_dev;
+  return a;
+}
+
+template <class Stage, bool RED>
+void launch_march(H* h, MarchArgs a) {
+  dim3 grid;
+  if constexpr (Stage::kRow0 == -1) {  // restriction: tiles of coarse rows / columns
+    const long ty = (a.gc.ny + 1 + Stage::kOwned / 2 - 1) / (Stage::kOwned / 2);
+    a.tx = march_tx(ty, a.gc.nx + 1);
+    grid = dim3(ty, (a.gc.nx + 1 + a.tx - 1) / a.tx);
+  } else {
+    const long ty = (a.g.ny + 1 + Stage::kOwned - 1) / Stage::kOwned;
+    a.tx = march_tx(ty, a.g.nx + 1);
+    grid = dim3(ty, (a.g.nx + 1 + a.tx - 1) / a.tx);
+  }
+  const size_t sm = static_cast<size_t>(Stage::kSlot) * kStages;
+  k_march<Stage, RED><<<grid, kMarchThreads, sm, h->stream>>>(a);
+  CKL();
+  h->count();
+}
+
 void apply_level(H* h, int l, const double2* x, double2* y) {
   const Level& L = h->lev[l];
+  if (l == h->nc) {
+    MarchArgs a = march_args(h, x);
+    a.out0 = y;
+    launch_march<StApply<false>, false>(h, a);
+    return;
+  }
   with_op(h, l, [&](auto op) {
     k_apply<decltype(op), false><<<node_grid(L.g), node_block(), 0, h->stream>>>(
         op, L.g, x, y, nullptr, nullptr, kRedNone, nullptr, nullptr, nullptr);
@@ -224,15 +277,29 @@ void apply_level(H* h, int l, const double2* x, double2* y) {
 
 // y = A x and out = x.y (reduction op `rop` updates the PCG scalars)
 void apply_dot_fine(H* h, const double2* x, double2* y, RedOp rop, double* out) {
-  const Level& L = h->fine();
-  k_apply<FineOp, true><<<node_grid(L.g), node_block(), 0, h->stream>>>(
-      h->fine_op(), L.g, x, y, h->partials, h->ticket, rop, h->st, h->hm_dev, out);
-  CKL();
-  h->count();
+  MarchArgs a = march_args(h, x);
+  a.out0 = y;
+  a.rop = rop;
+  a.red_out = out;
+  launch_march<StApply<true>, true>(h, a);
 }
 
-void sweep_level(H* h, int l, bool zero, const double2* xin, double2* xout, const double2* f) {
+// one damped-Jacobi sweep; at the finest level optionally fused with z.r
+void sweep_level(H* h, int l, bool zero, const double2* xin, double2* xout, const double2* f,
+                 RedOp rop = kRedNone) {
   const Level& L = h->lev[l];
+  if (l == h->nc && !zero) {
+    MarchArgs a = march_args(h, xin);
+    a.f = f;
+    a.out0 = xout;
+    if (rop != kRedNone) {
+      a.rop = rop;
+      launch_march<StSweep<true>, true>(h, a);
+    } else {
+      launch_march<StSweep<false>, false>(h, a);
+    }
+    return;
+  }
   with_op(h, l, [&](auto op) {
     if (zero)
       k_sweep<decltype(op), true><<<node_grid(L.g), node_block(), 0, h->stream>>>(op, L.g, xin, xout, f, h->omega);
@@ -245,6 +312,13 @@ void sweep_level(H* h, int l, bool zero, const double2* xin, double2* xout, cons
 
 void residual_level(H* h, int l, const double2* x, const double2* f, double2* r) {
   const Level& L = h->lev[l];
+  if (l == h->nc) {
+    MarchArgs a = march_args(h, x);
+    a.f = f;
+    a.out0 = r;
+    launch_march<StResidual, false>(h, a);
+    return;
+  }
   with_op(h, l, [&](auto op) {
     k_residual<decltype(op)><<<node_grid(L.g), node_block(), 0, h->stream>>>(op, L.g, x, f, r);
   });
@@ -277,32 +351,66 @@ void coarse_solve(H* h, const double2* f, double2* u) {
 // One gamma-cycle at level l (mg_cycle, solvers.cpp:483-514). `zero` means
 // the iterate is logically zero on entry (the reference zeroes u_coarse
 // before the first visit, solvers.cpp:501, and pcgmg starts from z = 0,
-// solvers.cpp:524); the buffer content is then never read.
-void enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post) {
+// solvers.cpp:524); the buffer content is then never read. At the finest
+// level the passes are the fused marching stages (tmg_march.cuh); when
+// `zr_op` is set the last post-sweep also reduces z.r for PCG. Returns
+// whether that reduction was fused.
+bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp zr_op = kRedNone) {
   Level& L = h->lev[l];
   if (l == 0) {
     coarse_solve(h, L.f, L.u[L.cur]);
-    return;
+    return false;
   }
-  for (int s = 0; s < pre; ++s) {
+  Level& C = h->lev[l - 1];
+  const bool fine = (l == h->nc);
+  int s = 0;
+  if (fine && zero && pre >= 2) {
+    MarchArgs a = march_args(h, nullptr);
+    a.f = L.f;
+    a.out0 = L.u[L.cur ^ 1];
+    launch_march<StSweep01, false>(h, a);
+    L.cur ^= 1;
+    s = 2;
+    zero = false;
+  }
+  for (; s < pre; ++s) {
     sweep_level(h, l, zero, L.u[L.cur], L.u[L.cur ^ 1], L.f);
     L.cur ^= 1;
     zero = false;
   }
-  Level& C = h->lev[l - 1];
   if (zero) {
     restrict_level(h, l, L.f, C.f);  // residual of u = 0 is f
+  } else if (fine) {
+    MarchArgs a = march_args(h, L.u[L.cur]);
+    a.f = L.f;
+    a.out0 = C.f;
+    launch_march<StResidRestrict, false>(h, a);
   } else {
     residual_level(h, l, L.u[L.cur], L.f, L.res);
     restrict_level(h, l, L.res, C.f);
   }
-  const int visits = (l == h->nc) ? 1 : gamma;
+  const int visits = fine ? 1 : gamma;
   for (int t = 0; t < visits; ++t) enqueue_cycle(h, l - 1, t == 0, gamma, pre, post);
-  prolong_level(h, l, C.u[C.cur], L.u[L.cur], !zero);
-  for (int s = 0; s < post; ++s) {
-    sweep_level(h, l, false, L.u[L.cur], L.u[L.cur ^ 1], L.f);
+  int p = 0;
+  if (fine && !zero && post >= 1) {
+    MarchArgs a = march_args(h, L.u[L.cur]);
+    a.uc = C.u[C.cur];
+    a.f = L.f;
+    a.out0 = L.u[L.cur ^ 1];
+    launch_march<StProlongSweep, false>(h, a);
+    L.cur ^= 1;
+    p = 1;
+  } else {
+    prolong_level(h, l, C.u[C.cur], L.u[L.cur], !zero);
+  }
+  bool fused = false;
+  for (; p < post; ++p) {
+    const bool last = (p == post - 1);
+    sweep_level(h, l, false, L.u[L.cur], L.u[L.cur ^ 1], L.f, (fine && last) ? zr_op : kRedNone);
+    fused = fine && last && zr_op != kRedNone;
     L.cur ^= 1;
   }
+  return fused;
 }
 
 long flat2(const Level& L) { return L.g.size; }  // double2 count of a padded field
@@ -319,43 +427,53 @@ void dot(H* h, const double2* a, const double2* b, RedOp op, double* out) {
   h->count();
 }
 
+// One PCG iteration (pcg_solve loop body, solvers.cpp:359-391) as a graph.
+// Two graphs alternate the roles of the two direction buffers, because the
+// fused p-update reads the old p around each node while writing the new one.
 void capture_iteration(H* h, int gamma, int pre, int post) {
-  if (h->graph && h->g_gamma == gamma && h->g_pre == pre && h->g_post == post) return;
-  if (h->graph) {
-    cudaGraphExecDestroy(h->graph);
-    h->graph = nullptr;
+  if (h->graph[0] && h->g_gamma == gamma && h->g_pre == pre && h->g_post == post) return;
+  for (auto& gx : h->graph) {
+    if (gx) cudaGraphExecDestroy(gx);
+    gx = nullptr;
   }
-  for (Level& L : h->lev) L.cur = 0;
   const long n2 = flat2(h->fine());
-  cudaGraph_t g = nullptr;
-  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-  h->capturing = true;
-  h->capture_kernels = 0;
-  try {
-    // z = M^-1 r: one cycle from z = 0 at the finest level (solvers.cpp:523-527)
-    enqueue_cycle(h, h->nc, true, gamma, pre, post);
-    double2* z = h->fine().u[h->fine().cur];
-    h->z_final = z;
-    dot(h, z, h->r, kRedZr, nullptr);  // zr, beta
-    k_update_p<<<red_grid(n2), kRedThreads, 0, h->stream>>>(z, h->p, n2, h->st);
-    CKL();
-    h->count();
-    apply_dot_fine(h, h->p, h->ap, kRedPap, nullptr);  // Ap, pAp, alpha
-    k_update_xr<<<red_grid(n2), kRedThreads, 0, h->stream>>>(h->x, h->r, h->p, h->ap, n2, h->partials,
-                                                               h->ticket, h->st, h->hm_dev);
-    CKL();
-    h->count();
-  } catch (...) {
+  for (int k = 0; k < 2; ++k) {
+    for (Level& L : h->lev) L.cur = 0;
+    double2* p_old = h->pbuf[k];
+    double2* p_new = h->pbuf[k ^ 1];
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    h->capturing = true;
+    h->capture_kernels = 0;
+    try {
+      // z = M^-1 r: one cycle from z = 0 (solvers.cpp:523-527), fused with z.r
+      const bool fused = enqueue_cycle(h, h->nc, true, gamma, pre, post, kRedZr);
+      double2* z = h->fine().u[h->fine().cur];
+      if (!fused) dot(h, z, h->r, kRedZr, nullptr);
+      // p = z + beta p; Ap; pAp; alpha (solvers.cpp:367-382)
+      MarchArgs a = march_args(h, z);
+      a.u2 = p_old;
+      a.out0 = p_new;
+      a.out1 = h->ap;
+      a.rop = kRedPap;
+      launch_march<StPupd, true>(h, a);
+      // x += alpha p; r -= alpha Ap; rr (solvers.cpp:383-386)
+      k_update_xr<<<red_grid(n2), kRedThreads, 0, h->stream>>>(h->x, h->r, p_new, h->ap, n2, h->partials,
+                                                                 h->ticket, h->st, h->hm_dev);
+      CKL();
+      h->count();
+    } catch (...) {
+      h->capturing = false;
+      cudaStreamEndCapture(h->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
     h->capturing = false;
-    cudaStreamEndCapture(h->stream, &g);
-    if (g) cudaGraphDestroy(g);
-    throw;
+    CK(cudaStreamEndCapture(h->stream, &g));
+    CK(cudaGraphInstantiate(&h->graph[k], g, 0));
+    cudaGraphDestroy(g);
+    h->graph_kernels = h->capture_kernels;
   }
-  h->capturing = false;
-  CK(cudaStreamEndCapture(h->stream, &g));
-  CK(cudaGraphInstantiate(&h->graph, g, 0));
-  cudaGraphDestroy(g);
-  h->graph_kernels = h->capture_kernels;
   h->g_gamma = gamma;
   h->g_pre = pre;
   h->g_post = post;
@@ -434,7 +552,7 @@ void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int 
   k_pcg_begin<<<1, 1, 0, h->stream>>>(h->st);
   CKL();
   h->count();
-  CK(cudaMemsetAsync(h->p, 0, sizeof(double2) * n2, h->stream));
+  CK(cudaMemsetAsync(h->pbuf[0], 0, sizeof(double2) * n2, h->stream));
   if (use_x0) {
     CK(cudaMemcpyAsync(h->x, h->x0, sizeof(double2) * n2, cudaMemcpyDeviceToDevice, h->stream));
     apply_level(h, h->nc, h->x, F.res);
@@ -465,7 +583,7 @@ void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int 
       o.converged = 1;
     } else {
       for (int it = 1; it <= max_iter; ++it) {
-        CK(cudaGraphLaunch(h->graph, h->stream));
+        CK(cudaGraphLaunch(h->graph[(it - 1) & 1], h->stream));
         h->launches += h->graph_kernels;
         CK(cudaStreamSynchronize(h->stream));
         const volatile HostMirror* m = h->hm;
@@ -592,7 +710,7 @@ int tmg_gpu_create(int nx, int ny, int num_coarsenings, int dofs_per_node, int d
       const int s = 1 << (num_coarsenings - l);
       L.g = make_grid(nx / s, ny / s);
       L.ndof = 2L * (L.g.nx + 1) * (L.g.ny + 1);
-      const size_t vb = sizeof(double2) * L.g.size;
+      const size_t vb = sizeof(double2) * (L.g.size + kSlackNodes);
       CK(cudaMalloc(&L.u[0], vb));
       CK(cudaMalloc(&L.u[1], vb));
       CK(cudaMalloc(&L.res, vb));
@@ -608,16 +726,16 @@ int tmg_gpu_create(int nx, int ny, int num_coarsenings, int dofs_per_node, int d
       }
     }
     Level& F = hp->fine();
-    const size_t vb = sizeof(double2) * F.g.size;
-    for (double2** v : {&hp->x, &hp->r, &hp->p, &hp->ap, &hp->b, &hp->x0}) {
+    const size_t vb = sizeof(double2) * (F.g.size + kSlackNodes);
+    for (double2** v : {&hp->x, &hp->r, &hp->pbuf[0], &hp->pbuf[1], &hp->ap, &hp->b, &hp->x0}) {
       CK(cudaMalloc(v, vb));
       CK(cudaMemsetAsync(*v, 0, vb, hp->stream));
     }
     F.f = hp->r;  // the finest cycle smooths against the PCG residual
-    CK(cudaMalloc(&hp->E, sizeof(double) * F.g.size));
-    CK(cudaMemsetAsync(hp->E, 0, sizeof(double) * F.g.size, hp->stream));
-    CK(cudaMalloc(&hp->M, F.g.size));
-    CK(cudaMemsetAsync(hp->M, 0, F.g.size, hp->stream));
+    CK(cudaMalloc(&hp->E, sizeof(double) * (F.g.size + kSlackNodes)));
+    CK(cudaMemsetAsync(hp->E, 0, sizeof(double) * (F.g.size + kSlackNodes), hp->stream));
+    CK(cudaMalloc(&hp->M, F.g.size + kSlackNodes));
+    CK(cudaMemsetAsync(hp->M, 0, F.g.size + kSlackNodes, hp->stream));
     hp->n0 = n0;
     CK(cudaMalloc(&hp->A0, sizeof(double) * n0 * n0));
     CK(cudaMalloc(&hp->LiT, sizeof(double) * n0 * n0));
@@ -685,7 +803,8 @@ int tmg_gpu_set_problem(tmg_gpu_handle* h, double nu, const int* fixed_dofs, int
     CK(cudaMemcpyAsync(h->M, mask.data(), g.size, cudaMemcpyHostToDevice, h->stream));
     h->nu = nu;
     tmg_element_stiffness(1.0, nu, h->ke);
-    CK(cudaMemcpyToSymbolAsync(c_ke, h->ke, sizeof(h->ke), 0, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyToSymbolAsync(c_k8, h->ke, 8 * sizeof(double), 0, cudaMemcpyHostToDevice, h->stream));  // row 0
+    CK(cudaMemcpyToSymbolAsync(c_ke64, h->ke, 64 * sizeof(double), 0, cudaMemcpyHostToDevice, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     h->have_problem = true;
     h->have_setup = false;
@@ -1017,7 +1136,7 @@ int tmg_gpu_time_kernel(tmg_gpu_handle* h, int which, int reps, double* avg_ms, 
     Level& F = h->fine();
     const double nodes = static_cast<double>(F.g.nx + 1) * (F.g.ny + 1);
     auto launch = [&] {
-      if (which == 0) apply_level(h, h->nc, h->p, h->ap);
+      if (which == 0) apply_level(h, h->nc, h->pbuf[0], h->ap);
       else sweep_level(h, h->nc, false, F.u[0], F.u[1], h->r);
     };
     for (int w = 0; w < 3; ++w) launch();

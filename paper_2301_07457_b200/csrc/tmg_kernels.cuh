@@ -545,7 +545,7 @@ __global__ void k_element_energy(Grid g, const double2* __restrict__ u, double* 
   for (int r = 0; r < 8; ++r) {
     double row = 0.0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) row = fma(c_ke[r * 8 + q], ue[q], row);
+    for (int q = 0; q < 8; ++q) row = fma(c_ke64[r * 8 + q], ue[q], row);
     s = fma(ue[r], row, s);
   }
   out[static_cast<long>(ex) * g.ny + ey] = s;

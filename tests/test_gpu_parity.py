@@ -74,7 +74,10 @@ def test_one_cycle_matches_mg_cycle(nx, ny, nc, gamma):
     for u0 in (np.zeros(sysc.n), rng.standard_normal(sysc.n)):
         got = P.mg_cycle(ops, u0, f, gamma, 2, 2)
         want = sysc.vcycle(f, u0, gamma, 2, 2)
-        assert rel(got, want) <= 1e-12
+        # the device Ke is the symmetric 8-value form of the quadrature Ke
+        # (<= 1 ulp per entry, tmg_device.cuh); one cycle amplifies that
+        # through the coarsest solve to ~1e-12 at 128^2
+        assert rel(got, want) <= 1e-11
 
 
 def test_transfer_properties():
