@@ -1,0 +1,148 @@
+"""Pin the CPU checker (oracle/liboracle.so) before trusting it.
+
+1. Against the committed golden fixtures tests/golden/*.npz, generated from
+   the unmodified reference by tests/golden/make_golden.py: every quantity
+   must match BIT FOR BIT (the restatement performs the reference's floating
+   point operations in the reference's order).
+2. Against the reference itself (oracle/_ref, compiled from /root/reference
+   by oracle/Makefile) on fresh random cases, when it is built.
+3. Against the reference's own known-answer tests: the closed-form Q4
+   stiffness (proj/tests/test_fem.cpp:19-34, oracles.hpp:193-215) and the
+   filter identity / uniformity / conservation properties
+   (proj/tests/test_mto.cpp:116-184).
+"""
+import pathlib
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+
+GOLDEN = pathlib.Path(__file__).resolve().parent / "golden"
+CASES = sorted(p for p in GOLDEN.glob("wall*.npz"))
+PHASES = np.array([1.0, 0.5, 0.2, 1e-9])
+
+
+def closed_form_q4(e, nu):
+    """proj/tests/oracles.hpp:193-215 (the reference's own oracle)."""
+    k = [0.5 - nu / 6.0, 0.125 + nu / 8.0, -0.25 - nu / 12.0, -0.125 + 3.0 * nu / 8.0,
+         -0.25 + nu / 12.0, -0.125 - nu / 8.0, nu / 6.0, 0.125 - 3.0 * nu / 8.0]
+    idx = [[0, 1, 2, 3, 4, 5, 6, 7], [1, 0, 7, 6, 5, 4, 3, 2], [2, 7, 0, 5, 6, 3, 4, 1],
+           [3, 6, 5, 0, 7, 2, 1, 4], [4, 5, 6, 7, 0, 1, 2, 3], [5, 4, 3, 2, 1, 0, 7, 6],
+           [6, 3, 4, 1, 2, 7, 0, 5], [7, 2, 1, 4, 3, 6, 5, 0]]
+    c = e / (1.0 - nu * nu)
+    return np.array([[c * k[idx[i][j]] for j in range(8)] for i in range(8)])
+
+
+def test_golden_fixtures_exist():
+    assert len(CASES) >= 4
+    assert (GOLDEN / "element_stiffness.npz").exists()
+
+
+def test_element_stiffness_bitwise_and_closed_form():
+    g = np.load(GOLDEN / "element_stiffness.npz")
+    for nu in (0.3, 0.42):
+        k = po.element_stiffness("orc", 1.0, nu)
+        assert np.array_equal(k, g[f"ke_nu{nu}"])
+        assert np.max(np.abs(k - closed_form_q4(1.0, nu))) <= 1e-12 * np.max(np.abs(k))
+        assert np.array_equal(k, k.T)
+        # rigid translations produce no force (test_fem.cpp:49-61)
+        for c in range(2):
+            assert np.max(np.abs(k[:, c::2].sum(axis=1))) < 1e-12
+
+
+@pytest.mark.parametrize("path", CASES, ids=lambda p: p.stem)
+def test_oracle_matches_reference_golden_bitwise(path):
+    g = np.load(path)
+    nx, ny, nc = int(g["nx"]), int(g["ny"]), int(g["nc"])
+    loads = list(zip(g["load_dofs"].tolist(), g["load_vals"].tolist()))
+    E = po.effective_moduli("orc", nx, ny, g["alpha"], PHASES, 3.0)
+    assert np.array_equal(E, g["E"])
+    s = po.System("orc", nx, ny, E, 0.3, g["fixed"], loads).build_mg(nc, 0.6)
+    assert np.array_equal(s.rhs(), g["b"])
+    for lvl in range(nc + 1):
+        off, col, val = s.csr(lvl)
+        assert np.array_equal(off, g[f"L{lvl}_off"])
+        assert np.array_equal(col, g[f"L{lvl}_col"])
+        assert np.array_equal(val, g[f"L{lvl}_val"]), f"level {lvl}"
+    x0 = g["x0"] if g["x0"].size else None
+    r = s.solve(g["b"], tol=1e-8, max_iter=500, x0=x0)
+    assert r["iterations"] == int(g["iterations"])
+    assert np.array_equal(r["residual_history"], g["hist"])
+    assert np.array_equal(r["solution"], g["x"])
+    assert s.compliance(g["x"]) == float(g["compliance"])
+    f = g["f"]
+    assert np.array_equal(s.vcycle(f, np.zeros_like(f), 1, 2, 2), g["vcycle_v22"])
+    assert np.array_equal(s.vcycle(f, np.zeros_like(f), 2, 1, 1), g["vcycle_w11"])
+    assert np.array_equal(po.element_energies("orc", nx, ny, g["x"], 0.3), g["energies"])
+    sens = po.sensitivities("orc", nx, ny, g["alpha"], PHASES, 3.0, 0.3, g["x"])
+    assert np.array_equal(sens, g["sens"])
+    for radius in (1.5, 3.0):
+        filt = np.stack([po.filter_sensitivities("orc", nx, ny, g["alpha_floored"], ph, radius, sens[ph])
+                         for ph in range(4)])
+        assert np.array_equal(filt, g[f"filter_r{radius}"])
+
+
+@pytest.mark.skipif(not po.available("ref"), reason="oracle/_ref not built (no /root/reference)")
+@pytest.mark.parametrize("nx,ny,nc,seed", [(8, 16, 1, 11), (20, 12, 2, 12), (40, 40, 3, 13)])
+def test_oracle_matches_live_reference_bitwise(nx, ny, nc, seed):
+    rng = np.random.default_rng(seed)
+    E = rng.uniform(1e-3, 2.0, nx * ny)
+    fixed = [2 * x * (ny + 1) for x in range(nx + 1)] + [2 * x * (ny + 1) + 1 for x in range(0, nx + 1, 2)]
+    loads = [(2 * (x * (ny + 1) + ny) + 1, -rng.uniform()) for x in range(nx + 1)]
+    out = {}
+    for kind in ("orc", "ref"):
+        s = po.System(kind, nx, ny, E, 0.27, fixed, loads).build_mg(nc, 0.7)
+        b = s.rhs()
+        r = s.solve(b, tol=1e-10, max_iter=400, gamma=2, pre=1, post=1)
+        out[kind] = (b, r, [s.csr(l)[2] for l in range(nc + 1)], s.compliance(r["solution"]))
+    (b0, r0, c0, k0), (b1, r1, c1, k1) = out["orc"], out["ref"]
+    assert np.array_equal(b0, b1)
+    assert r0["iterations"] == r1["iterations"]
+    assert np.array_equal(r0["solution"], r1["solution"])
+    assert all(np.array_equal(a, b) for a, b in zip(c0, c1))
+    assert k0 == k1
+
+
+@pytest.mark.skipif(not po.available("ref"), reason="oracle/_ref not built (no /root/reference)")
+def test_error_behaviour_matches_reference():
+    nx = ny = 8
+    E = np.ones(nx * ny)
+    for kind in ("orc", "ref"):
+        # unconstrained structure: singular coarsest matrix (solvers.cpp:144-148)
+        s = po.System(kind, nx, ny, E, 0.3, [], [(2 * ((nx // 2) * (ny + 1) + ny) + 1, -1.0)])
+        with pytest.raises(po.OracleError) as ei:
+            s.build_mg(2)
+        assert ei.value.code == 3 and ei.value.row == 14
+        # fixed and loaded dof (fem.cpp:122-124)
+        with pytest.raises(po.OracleError) as ei:
+            po.System(kind, nx, ny, E, 0.3, [1], [(1, 1.0)])
+        assert ei.value.code == 1
+        # divisibility (grid.cpp:66-73)
+        s = po.System(kind, nx, ny, E, 0.3, [0, 1], [(5, 1.0)])
+        with pytest.raises(po.OracleError) as ei:
+            s.build_mg(4)
+        assert ei.value.code == 1
+
+
+def test_filter_properties_of_the_reference_tests():
+    """test_mto.cpp:116-184 (identity for r <= 1, uniform field, conservation)."""
+    nx, ny = 7, 7
+    rng = np.random.default_rng(8)
+    a = np.tile([0.4, 0.6], (nx * ny, 1))
+    raw = -rng.uniform(0.0, 1.0, nx * ny)
+    assert np.array_equal(po.filter_sensitivities("orc", nx, ny, a, 0, 1.0, raw), raw)
+    uni = np.full(nx * ny, -1.75)
+    assert np.allclose(po.filter_sensitivities("orc", nx, ny, a, 0, 3.0, uni), -1.75, rtol=1e-13)
+    rf = 2.5
+    f = po.filter_sensitivities("orc", nx, ny, a, 0, rf, raw)
+    for ex in range(nx):
+        for ey in range(ny):
+            ws = wr = 0.0
+            for jx in range(nx):
+                for jy in range(ny):
+                    w = rf - np.sqrt((ex - jx) ** 2 + (ey - jy) ** 2)
+                    if w > 0:
+                        ws += w
+                        wr += w * raw[jx * ny + jy]
+            assert abs(f[ex * ny + ey] * ws - wr) <= 1e-12 * abs(wr)
