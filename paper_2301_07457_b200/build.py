@@ -60,9 +60,30 @@ def build_oracle(force: bool = False) -> None:
         subprocess.run(args + ["ref", f"REF_DIR={ref}"], check=True, stdout=subprocess.DEVNULL)
 
 
+def build_dropin(force: bool = False) -> None:
+    """tests/cpp/dropin_check: the reference's own optimizer types and loop
+    with the solve block served by include/topmg_gpu.hpp (test driver; needs
+    the reference objects of oracle/_ref, so it is built where they exist)."""
+    ref = pathlib.Path(os.environ.get("TOPMG_REF_DIR", "/root/reference/proj"))
+    objs = [ROOT / "oracle" / "_ref" / f"{s}.o" for s in ("sparse", "grid", "density", "fem", "solvers", "mto")]
+    if not (ref / "include").exists() or not all(o.exists() for o in objs):
+        return
+    src = ROOT / "tests" / "cpp" / "dropin_check.cpp"
+    out = ROOT / "tests" / "cpp" / "dropin_check"
+    lib = PKG / "libtmg_gpu.so"
+    deps = [src, lib, ROOT / "include" / "topmg_gpu.hpp", *objs]
+    if not force and not _stale(out, deps):
+        return
+    cmd = [shutil.which("g++") or "g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", f"-I{ref / 'include'}",
+           str(src), *map(str, objs), f"-L{PKG}", "-ltmg_gpu", "-Wl,-rpath,$ORIGIN/../../paper_2301_07457_b200",
+           "-o", str(out)]
+    subprocess.run(cmd, check=True)
+
+
 def build_all(force: bool = False) -> None:
     build_gpu(force)
     build_oracle(force)
+    build_dropin(force)
 
 
 if __name__ == "__main__":

@@ -1,0 +1,22 @@
+"""C++ drop-in check: the reference optimizer's designs solved by the
+reference and by include/topmg_gpu.hpp (tests/cpp/dropin_check.cpp)."""
+import pathlib
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+BIN = pathlib.Path(__file__).resolve().parent / "cpp" / "dropin_check"
+
+
+@pytest.mark.skipif(not BIN.exists(), reason="dropin_check is built where /root/reference exists")
+def test_cpp_dropin_matches_reference_on_optimizer_designs():
+    p = subprocess.run([str(BIN), "64", "6"], capture_output=True, text=True, timeout=600)
+    lines = [l.split() for l in p.stdout.strip().splitlines()]
+    assert len(lines) == 6, p.stdout + p.stderr
+    for k, it_ref, it_gpu, eu, ec, es, ef in lines:
+        assert abs(int(it_ref) - int(it_gpu)) <= 2
+        assert float(eu) <= 1e-8 and float(ec) <= 1e-9
+        assert float(es) <= 1e-8 and float(ef) <= 1e-8
+    assert p.returncode == 0, p.stdout + p.stderr
