@@ -31,15 +31,24 @@
 namespace tmg {
 
 constexpr int kOY = 8;
+constexpr int kGX = 2;  // ghost node columns on each side of a slab
 constexpr int kStencilPlanes = 19;
 
+// One level as stored by one rank: the rank owns global node columns
+// [x0, x0 + ncol) and stores them as local columns 0 .. ncol-1 with kGX ghost
+// columns on each side (halo of the neighbouring slab, or zeros at the global
+// boundary). A single-GPU level is the slab x0 = 0, ncol = nx + 1.
 struct Grid {
-  int nx, ny;  // elements
+  int nx, ny;  // global elements of the level
   int P;       // padded pitch (nodes)
-  long size;   // padded node count (nx + 3) * P
+  long size;   // padded node count (ncol + 2 kGX) * P
+  int x0;      // global node column of local column 0
+  int ncol;    // owned node columns
   __host__ __device__ __forceinline__ long idx(int x, int y) const {
-    return static_cast<long>(x + 1) * P + y + kOY;
+    return static_cast<long>(x + kGX) * P + y + kOY;
   }
+  __host__ __device__ __forceinline__ long own_begin() const { return static_cast<long>(kGX) * P; }
+  __host__ __device__ __forceinline__ long own_count() const { return static_cast<long>(ncol) * P; }
 };
 
 // Unit-modulus Q4 Ke (fem.cpp:131-169) has only 8 distinct values: row r is a

@@ -67,7 +67,9 @@ Grid make_grid(int nx, int ny) {
   // y in [-1, ny+1] at offset kOY; a multiple of 16 nodes keeps every column
   // start 16-byte aligned for the TMA bulk copies of the byte-wide mask
   g.P = ((ny + 2 + kOY) + 15) / 16 * 16;
-  g.size = static_cast<long>(nx + 3) * g.P;
+  g.x0 = 0;
+  g.ncol = nx + 1;
+  g.size = static_cast<long>(g.ncol + 2 * kGX) * g.P;
   return g;
 }
 
@@ -421,8 +423,11 @@ int red_grid(long n2) {
 }
 
 void dot(H* h, const double2* a, const double2* b, RedOp op, double* out) {
-  const long n2 = flat2(h->fine());
-  k_dot<<<red_grid(n2), kRedThreads, 0, h->stream>>>(a, b, n2, h->partials, h->ticket, op, h->st, h->hm_dev, out);
+  // owned columns only: ghost columns may hold a neighbour's halo
+  const Grid& g = h->fine().g;
+  const long o = g.own_begin(), n2 = g.own_count();
+  k_dot<<<red_grid(n2), kRedThreads, 0, h->stream>>>(a + o, b + o, n2, h->partials, h->ticket, op, h->st,
+                                                     h->hm_dev, out);
   CKL();
   h->count();
 }
@@ -458,7 +463,9 @@ void capture_iteration(H* h, int gamma, int pre, int post) {
       a.rop = kRedPap;
       launch_march<StPupd, true>(h, a);
       // x += alpha p; r -= alpha Ap; rr (solvers.cpp:383-386)
-      k_update_xr<<<red_grid(n2), kRedThreads, 0, h->stream>>>(h->x, h->r, p_new, h->ap, n2, h->partials,
+      const long o = h->fine().g.own_begin(), no = h->fine().g.own_count();
+      k_update_xr<<<red_grid(no), kRedThreads, 0, h->stream>>>(h->x + o, h->r + o, p_new + o, h->ap + o, no,
+                                                                 h->partials,
                                                                  h->ticket, h->st, h->hm_dev);
       CKL();
       h->count();
@@ -556,10 +563,12 @@ void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int 
   if (use_x0) {
     CK(cudaMemcpyAsync(h->x, h->x0, sizeof(double2) * n2, cudaMemcpyDeviceToDevice, h->stream));
     apply_level(h, h->nc, h->x, F.res);
-    k_sub<<<red_grid(n2), kRedThreads, 0, h->stream>>>(h->b, F.res, h->r, n2);
+    k_sub<<<red_grid(F.g.own_count()), kRedThreads, 0, h->stream>>>(h->b + F.g.own_begin(), F.res + F.g.own_begin(),
+                                                                   h->r + F.g.own_begin(), F.g.own_count());
   } else {
     CK(cudaMemsetAsync(h->x, 0, sizeof(double2) * n2, h->stream));
-    k_sub<<<red_grid(n2), kRedThreads, 0, h->stream>>>(h->b, nullptr, h->r, n2);
+    k_sub<<<red_grid(F.g.own_count()), kRedThreads, 0, h->stream>>>(h->b + F.g.own_begin(), nullptr,
+                                                                   h->r + F.g.own_begin(), F.g.own_count());
   }
   CKL();
   h->count();

@@ -137,7 +137,7 @@ __device__ __forceinline__ NodeIdx node_of_thread(const Grid& g) {
   NodeIdx n;
   n.y = blockIdx.x * kBX + threadIdx.x;
   n.x = blockIdx.y * kBY + threadIdx.y;
-  n.ok = (n.x <= g.nx) && (n.y <= g.ny);
+  n.ok = (n.x < g.ncol) && (n.y <= g.ny);
   return n;
 }
 
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(128) k_galerkin(Op fine, Grid fg, Grid cg, dou
                                                   long LSc) {
   const int Y = blockIdx.x * 32 + threadIdx.x;
   const int X = blockIdx.y * 4 + threadIdx.y;
-  if (X > cg.nx || Y > cg.ny) return;
+  if (X >= cg.ncol || Y > cg.ny) return;
   double acc[5][4];
 #pragma unroll
   for (int a = 0; a < 5; ++a)
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(128) k_galerkin(Op fine, Grid fg, Grid cg, dou
 #pragma unroll
     for (int dy = -1; dy <= 1; ++dy) {
       const int fx = 2 * X + dx, fy = 2 * Y + dy;
-      if (fx < 0 || fx > fg.nx || fy < 0 || fy > fg.ny) continue;
+      if (fg.x0 + fx < 0 || fg.x0 + fx > fg.nx || fy < 0 || fy > fg.ny) continue;  // global bounds
       const long i = fg.idx(fx, fy);
       const double wi = 0.25 * pw(dx) * pw(dy);
 #pragma unroll
@@ -345,7 +345,7 @@ template <class Op>
 __global__ void k_dense_assemble(Op op, Grid g, double* __restrict__ A, int n) {
   const int y = blockIdx.x * blockDim.x + threadIdx.x;
   const int x = blockIdx.y;
-  if (x > g.nx || y > g.ny) return;
+  if (x >= g.ncol || y > g.ny) return;
   const long i = g.idx(x, y);
   const int ri = 2 * (x * (g.ny + 1) + y);
   for (int ex = -1; ex <= 1; ++ex)

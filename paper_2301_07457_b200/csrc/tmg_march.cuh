@@ -435,7 +435,7 @@ struct StResidRestrict : WithF<-1> {
                              double2& acc) {
     __shared__ double2 rbuf[2][kTY];
     double2 r = make_double2(0.0, 0.0);
-    if (x >= 0 && x <= a.g.nx && yt >= 0 && yt <= a.g.ny) {
+    if (a.g.x0 + x >= 0 && a.g.x0 + x <= a.g.nx && yt >= 0 && yt <= a.g.ny) {  // global bounds
       double2 y, d;
       window_apply(L, C, R, y, d);
       const double2 f = fc(cs, mis, t);
@@ -566,14 +566,14 @@ template <class Stage>
 __device__ __forceinline__ void march_range(const MarchArgs& a, int& cf, int& cl, int& xlo, int& xhi) {
   if constexpr (Stage::kRow0 == -1) {
     const int X0 = blockIdx.y * a.tx;
-    const int X1 = min(X0 + a.tx, a.gc.nx + 1);
+    const int X1 = min(X0 + a.tx, a.gc.ncol);
     xlo = 2 * X0 - 1;
     xhi = 2 * X1 - 1;  // inclusive
     cf = xlo - 1;
     cl = xhi + 1;
   } else {
     xlo = blockIdx.y * a.tx;
-    xhi = min(xlo + a.tx, a.g.nx + 1) - 1;
+    xhi = min(xlo + a.tx, a.g.ncol) - 1;
     cf = xlo - 1 - Stage::kLead;
     cl = xhi + 1;
   }
@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(kMarchThreads) k_march(MarchArgs a) {
   march_range<Stage>(a, cf, cl, xlo, xhi);
   const int nent = cl - cf + 1;
   auto slot = [&](int j) { return smem_raw + static_cast<size_t>(j % kStages) * Stage::kSlot; };
-  auto in_storage = [&](int c) { return c >= -1 && c <= g.nx + 1; };
+  auto in_storage = [&](int c) { return c >= -kGX && c < g.ncol + kGX; };
 
   if (t == 0) {
     for (int s = 0; s < kStages; ++s) {
