@@ -63,6 +63,32 @@ typedef struct tmg_gpu_handle tmg_gpu_handle;
 int tmg_gpu_create(int nx, int ny, int num_coarsenings, int dofs_per_node,
                    int device, tmg_gpu_handle** out);
 void tmg_gpu_destroy(tmg_gpu_handle* h);
+
+/* ---- x-slab decomposition (multi-GPU) ---------------------------------- */
+/* The mesh is split into x-slabs: contiguous node-column ranges of the
+ * reference's column-major numbering (grid.hpp:19). Every level finer than
+ * `replicated_level` is distributed (one ghost column exchanged per pass, two
+ * before the fused restriction); levels 0..replicated_level are assembled on
+ * every rank and solved redundantly. replicated_level = -1 picks the finest
+ * level at which a slab would hold fewer than 16 node columns. Slab
+ * boundaries are multiples of 2^(num_coarsenings - replicated_level) fine
+ * columns. The PCG scalars are summed over ranks in rank order. */
+
+/* x0s[r] = first fine node column of rank r (nranks + 1 entries, the last is
+ * nx + 1); *rep_out = the replicated level used. Host-only. */
+int tmg_partition(int nx, int num_coarsenings, int nranks, int replicated_level, int* x0s, int* rep_out);
+/* One process, `nslabs` ranks on one device: the decomposition run end to end
+ * on a single GPU (halo exchange by device copies). */
+int tmg_gpu_create_local_slabs(int nx, int ny, int num_coarsenings, int dofs_per_node, int device, int nslabs,
+                               int replicated_level, tmg_gpu_handle** out);
+/* One rank per process (torchrun): exchanges by NCCL send/recv/broadcast and
+ * all-reduce over NVLink / NVSwitch. nccl_unique_id: the 128-byte
+ * ncclUniqueId created by rank 0 with tmg_nccl_unique_id and shared by the
+ * caller. Host vectors passed to this handle are global; each rank reads and
+ * writes only its own columns. */
+int tmg_gpu_create_nccl(int nx, int ny, int num_coarsenings, int dofs_per_node, int device, int nranks, int rank,
+                        const void* nccl_unique_id, int replicated_level, tmg_gpu_handle** out);
+int tmg_nccl_unique_id(void* out128);
 /* Message of the last failing call; *row = DefinitenessError::row or -1. */
 int tmg_gpu_last_error(tmg_gpu_handle* h, char* buf, int len, int* row);
 

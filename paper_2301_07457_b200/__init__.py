@@ -31,7 +31,9 @@ from .topmg import (  # noqa: F401
     element_stiffness,
     filter_sensitivities,
     mg_cycle,
+    nccl_unique_id,
     pcgmg_solve,
     sensitivities,
+    slab_partition,
     wall_boundary_conditions,
 )

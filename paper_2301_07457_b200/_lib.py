@@ -23,6 +23,12 @@ _H = C.c_void_p
 SIGNATURES = [
     ("tmg_gpu_create", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_H)]),
     ("tmg_gpu_destroy", None, [_H]),
+    ("tmg_partition", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _I, _I]),
+    ("tmg_gpu_create_local_slabs", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                             C.POINTER(_H)]),
+    ("tmg_gpu_create_nccl", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                      C.c_int, C.POINTER(_H)]),
+    ("tmg_nccl_unique_id", C.c_int, [C.c_void_p]),
     ("tmg_gpu_last_error", C.c_int, [_H, C.c_char_p, C.c_int, _I]),
     ("tmg_gpu_set_problem", C.c_int, [_H, C.c_double, _I, C.c_int]),
     ("tmg_gpu_set_moduli", C.c_int, [_H, _D, C.c_long, C.c_double]),

@@ -1,16 +1,28 @@
 // libtmg_gpu.so -- host orchestration of the B200 pCGMG solve behind the C ABI
-// of include/tmg_gpu.h. One handle = one GPU, one stream, all levels resident.
+// of include/tmg_gpu.h.
 //
-// Per outer iteration of the reference optimizer (mto.cpp:267-283) the work is
+// A handle drives one or more *ranks*. A rank owns an x-slab of every
+// distributed level (contiguous node columns of the reference's column-major
+// numbering, grid.hpp:19) plus kGX ghost columns per side, and a full copy of
+// every replicated (small) level. One process per GPU uses one local rank and
+// NCCL for the exchanges; a single process can also drive several ranks on
+// one device (LocalComm), which is how the decomposition is tested on one
+// B200. With one rank every level is global and nothing is exchanged.
+//
+// Per outer iteration of the reference optimizer (mto.cpp:267-283):
 //   setup : Galerkin hierarchy (K6) + coarsest factor/inverse (K7) on device
 //   solve : PCG (K8) preconditioned by one gamma-cycle (K1-K5, K7) per
 //           iteration; one PCG iteration is a captured CUDA graph, the host
 //           only reads a 40-byte mirror of the PCG scalars to run the
 //           reference's stopping test (solvers.cpp:388) and error checks.
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -21,7 +33,7 @@
 
 using namespace tmg;
 
-namespace {
+namespace tmgi {
 
 struct TmgError {
   int code;
@@ -46,8 +58,9 @@ struct TmgError {
   } while (0)
 
 struct Level {
-  Grid g{};
-  long ndof = 0;
+  Grid g{};         // as stored by this rank (slab or global)
+  bool dist = false;
+  long ndof = 0;    // global dofs of the level
   double2* u[2] = {nullptr, nullptr};  // iterate (ping-pong for Jacobi)
   double2* f = nullptr;                // right-hand side of this level
   double2* res = nullptr;              // residual scratch
@@ -57,36 +70,79 @@ struct Level {
 
 dim3 node_block() { return dim3(kBX, kBY); }
 dim3 node_grid(const Grid& g) {
-  return dim3((g.ny + 1 + kBX - 1) / kBX, (g.nx + 1 + kBY - 1) / kBY);
+  return dim3((g.ny + 1 + kBX - 1) / kBX, (g.ncol + kBY - 1) / kBY);
 }
 
-Grid make_grid(int nx, int ny) {
+Grid make_grid(int nx, int ny, int x0, int ncol) {
   Grid g;
   g.nx = nx;
   g.ny = ny;
   // y in [-1, ny+1] at offset kOY; a multiple of 16 nodes keeps every column
   // start 16-byte aligned for the TMA bulk copies of the byte-wide mask
   g.P = ((ny + 2 + kOY) + 15) / 16 * 16;
-  g.x0 = 0;
-  g.ncol = nx + 1;
-  g.size = static_cast<long>(g.ncol + 2 * kGX) * g.P;
+  g.x0 = x0;
+  g.ncol = ncol;
+  g.size = static_cast<long>(ncol + 2 * kGX) * g.P;
   return g;
 }
 
-}  // namespace
+// ---------------------------------------------------------------- NCCL ------
+// libnccl is bound at run time (the process may already hold torch's copy of
+// libnccl.so.2; dlopen then returns that same library).
+struct NcclApi {
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclBroadcast) broadcast = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+};
 
-struct tmg_gpu_handle {
-  int device = 0;
-  cudaStream_t stream = nullptr;
+const NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (lib) {
+      api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(lib, "ncclGetUniqueId"));
+      api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(lib, "ncclCommInitRank"));
+      api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(lib, "ncclCommDestroy"));
+      api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(lib, "ncclAllReduce"));
+      api.broadcast = reinterpret_cast<decltype(api.broadcast)>(dlsym(lib, "ncclBroadcast"));
+      api.send = reinterpret_cast<decltype(api.send)>(dlsym(lib, "ncclSend"));
+      api.recv = reinterpret_cast<decltype(api.recv)>(dlsym(lib, "ncclRecv"));
+      api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(lib, "ncclGroupStart"));
+      api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(lib, "ncclGroupEnd"));
+      api.errorString = reinterpret_cast<decltype(api.errorString)>(dlsym(lib, "ncclGetErrorString"));
+    }
+  }
+  if (!api.commInitRank) fail(TMG_ERR_NCCL, "libnccl.so.2 not available");
+  return api;
+}
+
+#define NK(call)                                                                      \
+  do {                                                                                \
+    ncclResult_t r_ = (call);                                                         \
+    if (r_ != ncclSuccess) fail(TMG_ERR_NCCL, std::string(#call) + ": " + nccl().errorString(r_)); \
+  } while (0)
+
+}  // namespace tmgi
+using namespace tmgi;
+
+// ------------------------------------------------------------------ rank ----
+
+struct Rank {
+  int index = 0;  // global rank
   int nx = 0, ny = 0, nc = 0;
   std::vector<Level> lev;  // lev[0] coarsest ... lev[nc] finest (grid.hpp:47)
   double* E = nullptr;
   uint8_t* M = nullptr;
-  double nu = 0.3;
-  double ke[64];
-  bool have_problem = false, have_moduli = false, have_setup = false;
-  double omega = 0.6;
-  // coarsest level (K7)
+  // coarsest level (K7), replicated on every rank
   int n0 = 0;
   double *A0 = nullptr, *LiT = nullptr, *Ainv = nullptr;
   int* bad_row = nullptr;
@@ -98,14 +154,8 @@ struct tmg_gpu_handle {
   PcgState* st = nullptr;
   HostMirror* hm = nullptr;      // pinned, mapped
   HostMirror* hm_dev = nullptr;  // device alias of hm
-  double* scal = nullptr;        // device scalar for plain dots
+  double* scal = nullptr;        // device scalars: [0] result, [1] rank partial, [2] global sum
   double* scal_host = nullptr;   // pinned
-  bool have_solution = false;
-  // captured PCG iteration
-  cudaGraphExec_t graph[2] = {nullptr, nullptr};
-  int g_gamma = -1, g_pre = -1, g_post = -1;
-  long graph_kernels = 0;
-  double2* z_final = nullptr;
   // scratch for consumers
   double* dense = nullptr;
   long dense_cap = 0;
@@ -113,8 +163,169 @@ struct tmg_gpu_handle {
   long aux_cap = 0;
   double* aux2 = nullptr;
   long aux2_cap = 0;
-  int* iaux = nullptr;
-  long iaux_cap = 0;
+
+  Level& fine() { return lev[nc]; }
+  FineOp fine_op() const { return FineOp{E, M, lev[nc].g.P}; }
+  StencilOp stencil_op(int l) const { return StencilOp{lev[l].S, lev[l].g.size, lev[l].g.P}; }
+};
+
+namespace tmgi {
+
+// Halo exchange and all-reduce between the ranks of one solve.
+struct Comm {
+  virtual ~Comm() = default;
+  // ghost columns of a distributed level: `wl` columns on the left from the
+  // left neighbour's last owned columns, `wr` on the right from the right
+  // neighbour's first ones; a node column is P elements of `esize` bytes
+  // starting at field(rank).
+  virtual void halo(std::vector<Rank*>& rs, int level, const std::function<void*(Rank&)>& field, size_t esize,
+                    int wl, int wr, cudaStream_t s) = 0;
+  // owned column ranges [X0_r, X0_r + n_r) of a replicated level's planes
+  // (plane stride in elements) from every rank to every rank's full copy
+  virtual void gather_columns(std::vector<Rank*>& rs, int level, const std::function<void*(Rank&)>& field,
+                              size_t esize, long plane_stride, int planes, const std::vector<int>& X0,
+                              const std::vector<int>& ncol, cudaStream_t s) = 0;
+  // scal[1] of every rank summed into scal[2] of every rank (rank order)
+  virtual void allreduce(std::vector<Rank*>& rs, cudaStream_t s) = 0;
+  virtual bool local() const = 0;
+};
+
+// Several ranks in this process, all on the same device and stream.
+struct LocalComm : Comm {
+  const double** d_parts = nullptr;
+  double** d_outs = nullptr;
+  int n = 0;
+  explicit LocalComm(std::vector<Rank*>& rs) {
+    n = static_cast<int>(rs.size());
+    std::vector<const double*> p(n);
+    std::vector<double*> o(n);
+    for (int i = 0; i < n; ++i) {
+      p[i] = rs[i]->scal + 1;
+      o[i] = rs[i]->scal + 2;
+    }
+    CK(cudaMalloc(&d_parts, sizeof(double*) * n));
+    CK(cudaMalloc(&d_outs, sizeof(double*) * n));
+    CK(cudaMemcpy(d_parts, p.data(), sizeof(double*) * n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_outs, o.data(), sizeof(double*) * n, cudaMemcpyHostToDevice));
+  }
+  ~LocalComm() override {
+    cudaFree(d_parts);
+    cudaFree(d_outs);
+  }
+  bool local() const override { return true; }
+  void halo(std::vector<Rank*>& rs, int level, const std::function<void*(Rank&)>& field, size_t esize, int wl,
+            int wr, cudaStream_t s) override {
+    for (size_t i = 0; i < rs.size(); ++i) {
+      Rank& me = *rs[i];
+      const Grid& g = me.lev[level].g;
+      const size_t col = esize * g.P;
+      char* mine = static_cast<char*>(field(me));
+      if (i > 0 && wl > 0) {
+        Rank& L = *rs[i - 1];
+        const Grid& gl = L.lev[level].g;
+        char* src = static_cast<char*>(field(L)) + (gl.ncol + kGX - wl) * esize * gl.P;
+        CK(cudaMemcpyAsync(mine + (kGX - wl) * col, src, wl * col, cudaMemcpyDeviceToDevice, s));
+      }
+      if (i + 1 < rs.size() && wr > 0) {
+        Rank& R = *rs[i + 1];
+        char* src = static_cast<char*>(field(R)) + kGX * esize * R.lev[level].g.P;
+        CK(cudaMemcpyAsync(mine + (kGX + g.ncol) * col, src, wr * col, cudaMemcpyDeviceToDevice, s));
+      }
+    }
+  }
+  void gather_columns(std::vector<Rank*>& rs, int level, const std::function<void*(Rank&)>& field, size_t esize,
+                      long plane_stride, int planes, const std::vector<int>& X0, const std::vector<int>& ncol,
+                      cudaStream_t s) override {
+    for (size_t src = 0; src < rs.size(); ++src) {
+      const long P = rs[src]->lev[level].g.P;
+      for (size_t dst = 0; dst < rs.size(); ++dst) {
+        if (dst == src) continue;
+        for (int k = 0; k < planes; ++k) {
+          const size_t off = (k * plane_stride + static_cast<long>(X0[src] + kGX) * P) * esize;
+          CK(cudaMemcpyAsync(static_cast<char*>(field(*rs[dst])) + off, static_cast<char*>(field(*rs[src])) + off,
+                             ncol[src] * P * esize, cudaMemcpyDeviceToDevice, s));
+        }
+      }
+    }
+  }
+  void allreduce(std::vector<Rank*>&, cudaStream_t s) override {
+    k_sum_ranks<<<1, 1, 0, s>>>(d_parts, n, d_outs);
+    CKL();
+  }
+};
+
+// One rank per process, NCCL over NVLink / NVSwitch.
+struct NcclComm : Comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  NcclComm(int nranks_, int rank_, const void* id) : rank(rank_), nranks(nranks_) {
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    NK(nccl().commInitRank(&comm, nranks, uid, rank));
+  }
+  ~NcclComm() override {
+    if (comm) nccl().commDestroy(comm);
+  }
+  bool local() const override { return false; }
+  void halo(std::vector<Rank*>& rs, int level, const std::function<void*(Rank&)>& field, size_t esize, int wl,
+            int wr, cudaStream_t s) override {
+    Rank& me = *rs[0];
+    const Grid& g = me.lev[level].g;
+    const size_t col = esize * g.P;
+    char* mine = static_cast<char*>(field(me));
+    NK(nccl().groupStart());
+    if (rank > 0) {
+      // my first wr columns to the left neighbour's right ghost; its last wl to my left ghost
+      if (wr > 0) NK(nccl().send(mine + kGX * col, wr * col, ncclChar, rank - 1, comm, s));
+      if (wl > 0) NK(nccl().recv(mine + (kGX - wl) * col, wl * col, ncclChar, rank - 1, comm, s));
+    }
+    if (rank + 1 < nranks) {
+      if (wl > 0) NK(nccl().send(mine + (g.ncol + kGX - wl) * col, wl * col, ncclChar, rank + 1, comm, s));
+      if (wr > 0) NK(nccl().recv(mine + (kGX + g.ncol) * col, wr * col, ncclChar, rank + 1, comm, s));
+    }
+    NK(nccl().groupEnd());
+  }
+  void gather_columns(std::vector<Rank*>& rs, int level, const std::function<void*(Rank&)>& field, size_t esize,
+                      long plane_stride, int planes, const std::vector<int>& X0, const std::vector<int>& ncol,
+                      cudaStream_t s) override {
+    Rank& me = *rs[0];
+    const long P = me.lev[level].g.P;
+    char* buf = static_cast<char*>(field(me));
+    NK(nccl().groupStart());
+    for (int src = 0; src < nranks; ++src)
+      for (int k = 0; k < planes; ++k) {
+        char* p = buf + (k * plane_stride + static_cast<long>(X0[src] + kGX) * P) * esize;
+        NK(nccl().broadcast(p, p, ncol[src] * P * esize, ncclChar, src, comm, s));
+      }
+    NK(nccl().groupEnd());
+  }
+  void allreduce(std::vector<Rank*>& rs, cudaStream_t s) override {
+    NK(nccl().allReduce(rs[0]->scal + 1, rs[0]->scal + 2, 1, ncclDouble, ncclSum, comm, s));
+  }
+};
+
+}  // namespace tmgi
+
+// --------------------------------------------------------------- handle -----
+
+struct tmg_gpu_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int nx = 0, ny = 0, nc = 0;
+  int nranks = 1;  // global
+  int rep = 0;     // levels 0..rep are replicated on every rank
+  std::vector<int> xpart;  // fine node-column partition, nranks + 1 entries
+  std::vector<std::unique_ptr<Rank>> own;
+  std::vector<Rank*> ranks;  // ranks driven by this process
+  std::unique_ptr<Comm> comm;
+  double nu = 0.3;
+  double ke[64];
+  bool have_problem = false, have_moduli = false, have_setup = false, have_solution = false;
+  double omega = 0.6;
+  // captured PCG iteration
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  int g_gamma = -1, g_pre = -1, g_post = -1;
+  long graph_kernels = 0;
   // instrumentation
   long launches = 0;
   bool capturing = false;
@@ -125,23 +336,65 @@ struct tmg_gpu_handle {
   std::string err;
   int err_row = -1;
 
-  Level& fine() { return lev[nc]; }
+  bool multi() const { return nranks > 1; }
+  bool dist(int l) const { return nranks > 1 && l > rep; }
   void count(long k = 1) {
     if (capturing) capture_kernels += k;
     else launches += k;
   }
-  FineOp fine_op() const { return FineOp{E, M, lev[nc].g.P}; }
-  StencilOp stencil_op(int l) const { return StencilOp{lev[l].S, lev[l].g.size, lev[l].g.P}; }
 };
 
 namespace {
 
 using H = tmg_gpu_handle;
 
-template <class F>
-void with_op(H* h, int l, F&& fn) {
-  if (l == h->nc) fn(h->fine_op());
-  else fn(h->stencil_op(l));
+// ------------------------------------------------------------- geometry ----
+
+// Fine node-column partition: boundaries multiples of 2^(nc - rep) so every
+// distributed level has even slab boundaries.
+std::vector<int> partition(int nx, int nc, int rep, int nranks) {
+  std::vector<int> xp(nranks + 1, 0);
+  const long gran = 1L << (nc - rep);
+  for (int r = 1; r < nranks; ++r) {
+    const double target = static_cast<double>(r) * (nx + 1) / nranks;
+    xp[r] = static_cast<int>(std::llround(target / gran) * gran);
+  }
+  xp[nranks] = nx + 1;
+  return xp;
+}
+
+// highest replicated level: distribute level l while every rank owns >= 16
+// node columns of it
+int auto_rep(int nx, int nc, int nranks) {
+  if (nranks <= 1) return nc;
+  int rep = nc;
+  for (int l = nc; l >= 1; --l) {
+    const int cols = (nx >> (nc - l)) + 1;
+    if (cols / nranks >= 16) rep = l - 1;
+    else break;
+  }
+  return rep;
+}
+
+// owned node columns of rank r at level l (distributed-level geometry)
+void slab_cols(const H* h, int r, int l, int& x0, int& n) {
+  const int s = h->nc - l;
+  const int nxl = h->nx >> s;
+  x0 = h->xpart[r] >> s;
+  const int x1 = (r + 1 == h->nranks) ? nxl + 1 : (h->xpart[r + 1] >> s);
+  n = x1 - x0;
+}
+
+// A replicated level seen as the slab rank r's distributed parent level
+// writes / reads: same pitch, base offset X0 columns.
+Grid slab_view(const H* h, const Rank& R, int l, long& off) {
+  int x0, n;
+  slab_cols(h, R.index, l, x0, n);
+  Grid g = R.lev[l].g;
+  g.x0 = x0;
+  g.ncol = n;
+  off = static_cast<long>(x0) * g.P;
+  return g;
 }
 
 double* grow(double*& p, long& cap, long need) {
@@ -155,21 +408,21 @@ double* grow(double*& p, long& cap, long need) {
   return p;
 }
 
-void upload_nodes(H* h, double2* d, const double* host, const Grid& g) {
-  CK(cudaMemcpy2DAsync(d + g.idx(0, 0), sizeof(double2) * g.P, host, sizeof(double2) * (g.ny + 1),
-                       sizeof(double2) * (g.ny + 1), g.nx + 1, cudaMemcpyHostToDevice, h->stream));
+// host vector in reference layout <-> owned columns of the level on a rank
+void upload_nodes(cudaStream_t s, double2* d, const double* host, const Grid& g) {
+  CK(cudaMemcpy2DAsync(d + g.idx(0, 0), sizeof(double2) * g.P, host + 2L * g.x0 * (g.ny + 1),
+                       sizeof(double2) * (g.ny + 1), sizeof(double2) * (g.ny + 1), g.ncol, cudaMemcpyHostToDevice,
+                       s));
 }
 
-void download_nodes(H* h, double* host, const double2* d, const Grid& g) {
-  CK(cudaMemcpy2DAsync(host, sizeof(double2) * (g.ny + 1), d + g.idx(0, 0), sizeof(double2) * g.P,
-                       sizeof(double2) * (g.ny + 1), g.nx + 1, cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
+void download_nodes(cudaStream_t s, double* host, const double2* d, const Grid& g) {
+  CK(cudaMemcpy2DAsync(host + 2L * g.x0 * (g.ny + 1), sizeof(double2) * (g.ny + 1), d + g.idx(0, 0),
+                       sizeof(double2) * g.P, sizeof(double2) * (g.ny + 1), g.ncol, cudaMemcpyDeviceToHost, s));
 }
 
 void check_level(H* h, int level) {
   if (level < 0 || level > h->nc) {
-    fail(TMG_ERR_DIMENSION, "level " + std::to_string(level) + " outside [0, " +
-                                std::to_string(h->nc) + "]");
+    fail(TMG_ERR_DIMENSION, "level " + std::to_string(level) + " outside [0, " + std::to_string(h->nc) + "]");
   }
 }
 
@@ -177,40 +430,37 @@ void need_setup(H* h) {
   if (!h->have_setup) fail(TMG_ERR_DIMENSION, "multigrid operators not built (call tmg_gpu_set_moduli)");
 }
 
-void free_handle(H* h) {
-  cudaSetDevice(h->device);
-  for (cudaGraphExec_t gx : h->graph)
-    if (gx) cudaGraphExecDestroy(gx);
-  for (Level& L : h->lev) {
+void need_single(H* h, const char* what) {
+  if (h->multi()) fail(TMG_ERR_CONFIG, std::string(what) + " is available on single-rank handles only");
+}
+
+void free_rank(Rank& R) {
+  for (Level& L : R.lev) {
     cudaFree(L.u[0]);
     cudaFree(L.u[1]);
     cudaFree(L.res);
     cudaFree(L.S);
-    if (&L != &h->lev.back()) cudaFree(L.f);
+    if (&L != &R.lev.back()) cudaFree(L.f);
   }
-  cudaFree(h->E);
-  cudaFree(h->M);
-  cudaFree(h->A0);
-  cudaFree(h->LiT);
-  cudaFree(h->Ainv);
-  cudaFree(h->bad_row);
-  cudaFree(h->x);
-  cudaFree(h->r);
-  cudaFree(h->pbuf[0]);
-  cudaFree(h->pbuf[1]);
-  cudaFree(h->ap);
-  cudaFree(h->b);
-  cudaFree(h->x0);
-  cudaFree(h->partials);
-  cudaFree(h->ticket);
-  cudaFree(h->st);
-  cudaFree(h->scal);
-  cudaFree(h->dense);
-  cudaFree(h->aux);
-  cudaFree(h->aux2);
-  cudaFree(h->iaux);
-  if (h->hm) cudaFreeHost(h->hm);
-  if (h->scal_host) cudaFreeHost(h->scal_host);
+  for (void* p : {static_cast<void*>(R.E), static_cast<void*>(R.M), static_cast<void*>(R.A0),
+                  static_cast<void*>(R.LiT), static_cast<void*>(R.Ainv), static_cast<void*>(R.bad_row),
+                  static_cast<void*>(R.x), static_cast<void*>(R.r), static_cast<void*>(R.ap),
+                  static_cast<void*>(R.b), static_cast<void*>(R.x0), static_cast<void*>(R.pbuf[0]),
+                  static_cast<void*>(R.pbuf[1]), static_cast<void*>(R.partials), static_cast<void*>(R.ticket),
+                  static_cast<void*>(R.st), static_cast<void*>(R.scal), static_cast<void*>(R.dense),
+                  static_cast<void*>(R.aux), static_cast<void*>(R.aux2)})
+    cudaFree(p);
+  if (R.hm) cudaFreeHost(R.hm);
+  if (R.scal_host) cudaFreeHost(R.scal_host);
+}
+
+void free_handle(H* h) {
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (cudaGraphExec_t gx : h->graph)
+    if (gx) cudaGraphExecDestroy(gx);
+  h->comm.reset();
+  for (Rank* R : h->ranks) free_rank(*R);
   for (cudaEvent_t e : h->ev)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : h->uev)
@@ -218,7 +468,102 @@ void free_handle(H* h) {
   if (h->stream) cudaStreamDestroy(h->stream);
 }
 
-// ------------------------------------------------------------ launches --
+void alloc_rank(H* h, Rank& R) {
+  cudaStream_t s = h->stream;
+  R.nx = h->nx;
+  R.ny = h->ny;
+  R.nc = h->nc;
+  R.lev.resize(h->nc + 1);
+  for (int l = 0; l <= h->nc; ++l) {
+    Level& L = R.lev[l];
+    const int sh = h->nc - l;
+    const int nxl = h->nx >> sh, nyl = h->ny >> sh;
+    L.dist = h->dist(l);
+    int x0 = 0, n = nxl + 1;
+    if (L.dist) slab_cols(h, R.index, l, x0, n);
+    L.g = make_grid(nxl, nyl, x0, n);
+    L.ndof = 2L * (nxl + 1) * (nyl + 1);
+    const size_t vb = sizeof(double2) * (L.g.size + kSlackNodes);
+    for (double2** v : {&L.u[0], &L.u[1], &L.res}) {
+      CK(cudaMalloc(v, vb));
+      CK(cudaMemsetAsync(*v, 0, vb, s));
+    }
+    if (l < h->nc) {
+      CK(cudaMalloc(&L.f, vb));
+      CK(cudaMemsetAsync(L.f, 0, vb, s));
+      const size_t sb = sizeof(double) * (kStencilPlanes * L.g.size + kSlackNodes);
+      CK(cudaMalloc(&L.S, sb));
+      CK(cudaMemsetAsync(L.S, 0, sb, s));
+    }
+  }
+  Level& F = R.fine();
+  const size_t vb = sizeof(double2) * (F.g.size + kSlackNodes);
+  for (double2** v : {&R.x, &R.r, &R.pbuf[0], &R.pbuf[1], &R.ap, &R.b, &R.x0}) {
+    CK(cudaMalloc(v, vb));
+    CK(cudaMemsetAsync(*v, 0, vb, s));
+  }
+  F.f = R.r;  // the finest cycle smooths against the PCG residual
+  CK(cudaMalloc(&R.E, sizeof(double) * (F.g.size + kSlackNodes)));
+  CK(cudaMemsetAsync(R.E, 0, sizeof(double) * (F.g.size + kSlackNodes), s));
+  CK(cudaMalloc(&R.M, F.g.size + kSlackNodes));
+  CK(cudaMemsetAsync(R.M, 0, F.g.size + kSlackNodes, s));
+  const Grid& g0 = R.lev[0].g;
+  R.n0 = 2 * (g0.nx + 1) * (g0.ny + 1);
+  const size_t n0sq = sizeof(double) * R.n0 * R.n0;
+  CK(cudaMalloc(&R.A0, n0sq));
+  CK(cudaMalloc(&R.LiT, n0sq));
+  CK(cudaMalloc(&R.Ainv, n0sq));
+  CK(cudaMalloc(&R.bad_row, sizeof(int)));
+  const dim3 ng = node_grid(F.g);
+  const long nparts = std::max<long>(static_cast<long>(ng.x) * ng.y, kRedBlocks);
+  CK(cudaMalloc(&R.partials, sizeof(double) * nparts));
+  CK(cudaMalloc(&R.ticket, sizeof(unsigned)));
+  CK(cudaMemsetAsync(R.ticket, 0, sizeof(unsigned), s));
+  CK(cudaMalloc(&R.st, sizeof(PcgState)));
+  CK(cudaMemsetAsync(R.st, 0, sizeof(PcgState), s));
+  CK(cudaMalloc(&R.scal, 4 * sizeof(double)));
+  CK(cudaMemsetAsync(R.scal, 0, 4 * sizeof(double), s));
+  CK(cudaHostAlloc(&R.hm, sizeof(HostMirror), cudaHostAllocMapped));
+  std::memset(R.hm, 0, sizeof(HostMirror));
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.hm_dev), R.hm, 0));
+  CK(cudaHostAlloc(&R.scal_host, 4 * sizeof(double), cudaHostAllocDefault));
+}
+
+// ------------------------------------------------------------- exchanges ---
+
+void halo_vec(H* h, int l, const std::function<double2*(Rank&)>& field, int wl = 1, int wr = 1) {
+  if (!h->dist(l)) return;
+  h->comm->halo(h->ranks, l, [&](Rank& R) -> void* { return field(R); }, sizeof(double2), wl, wr, h->stream);
+}
+
+// replicated level l: every rank's owned columns to all ranks
+void gather_level(H* h, int l, const std::function<void*(Rank&)>& field, size_t esize, long plane_stride,
+                  int planes) {
+  std::vector<int> X0(h->nranks), n(h->nranks);
+  for (int r = 0; r < h->nranks; ++r) slab_cols(h, r, l, X0[r], n[r]);
+  h->comm->gather_columns(h->ranks, l, field, esize, plane_stride, planes, X0, n, h->stream);
+}
+
+// ---------------------------------------------------------- reductions ----
+
+// Launch a reduction on every rank: single rank -> the kernel's last block
+// applies `op`; several ranks -> partials, all-reduce, then k_scalar.
+void reduce(H* h, RedOp op, const std::function<void(Rank&, RedOp, double*)>& launch, bool want_out = false) {
+  if (!h->multi()) {
+    Rank& R = *h->ranks[0];
+    launch(R, op, want_out ? R.scal : nullptr);
+    return;
+  }
+  for (Rank* R : h->ranks) launch(*R, kRedPlain, R->scal + 1);
+  h->comm->allreduce(h->ranks, h->stream);
+  for (Rank* R : h->ranks) {
+    k_scalar<<<1, 1, 0, h->stream>>>(op, R->scal + 2, R->st, R->hm_dev, want_out ? R->scal : nullptr);
+    CKL();
+  }
+  h->count(static_cast<long>(h->ranks.size()) + (h->comm->local() ? 1 : 0));
+}
+
+// ------------------------------------------------------------ launches ----
 
 // output columns per marching CTA: long strips amortise the prologue; short
 // ones keep small grids spread over all 148 SMs
@@ -227,20 +572,26 @@ int march_tx(long rows_tiles, long cols) {
   return static_cast<int>(std::min<long>(64, std::max<long>(6, want)));
 }
 
-MarchArgs march_args(H* h, const double2* u) {
+MarchArgs march_args(H* h, Rank& R, const double2* u) {
   MarchArgs a{};
-  a.g = h->fine().g;
-  if (h->nc > 0) a.gc = h->lev[h->nc - 1].g;
+  a.g = R.fine().g;
   a.u = u;
-  a.E = h->E;
-  a.M = h->M;
+  a.E = R.E;
+  a.M = R.M;
   a.omega = h->omega;
-  a.partials = h->partials;
-  a.ticket = h->ticket;
+  a.partials = R.partials;
+  a.ticket = R.ticket;
   a.rop = kRedNone;
-  a.st = h->st;
-  a.hm = h->hm_dev;
+  a.st = R.st;
+  a.hm = R.hm_dev;
   return a;
+}
+
+// Grid + base offset of the coarse level l-1 as level l's kernels address it
+Grid coarse_of(H* h, Rank& R, int l, long& off) {
+  off = 0;
+  if (h->dist(l) && !h->dist(l - 1)) return slab_view(h, R, l - 1, off);
+  return R.lev[l - 1].g;
 }
 
 template <class Stage, bool RED>
@@ -248,12 +599,12 @@ void launch_march(H* h, MarchArgs a) {
   dim3 grid;
   if constexpr (Stage::kRow0 == -1) {  // restriction: tiles of coarse rows / columns
     const long ty = (a.gc.ny + 1 + Stage::kOwned / 2 - 1) / (Stage::kOwned / 2);
-    a.tx = march_tx(ty, a.gc.nx + 1);
-    grid = dim3(ty, (a.gc.nx + 1 + a.tx - 1) / a.tx);
+    a.tx = march_tx(ty, a.gc.ncol);
+    grid = dim3(ty, (a.gc.ncol + a.tx - 1) / a.tx);
   } else {
     const long ty = (a.g.ny + 1 + Stage::kOwned - 1) / Stage::kOwned;
-    a.tx = march_tx(ty, a.g.nx + 1);
-    grid = dim3(ty, (a.g.nx + 1 + a.tx - 1) / a.tx);
+    a.tx = march_tx(ty, a.g.ncol);
+    grid = dim3(ty, (a.g.ncol + a.tx - 1) / a.tx);
   }
   const size_t sm = static_cast<size_t>(Stage::kSlot) * kStages;
   k_march<Stage, RED><<<grid, kMarchThreads, sm, h->stream>>>(a);
@@ -261,15 +612,21 @@ void launch_march(H* h, MarchArgs a) {
   h->count();
 }
 
-void apply_level(H* h, int l, const double2* x, double2* y) {
-  const Level& L = h->lev[l];
-  if (l == h->nc) {
-    MarchArgs a = march_args(h, x);
+template <class F>
+void with_op(Rank& R, int l, F&& fn) {
+  if (l == R.nc) fn(R.fine_op());
+  else fn(R.stencil_op(l));
+}
+
+void apply_level(H* h, Rank& R, int l, const double2* x, double2* y) {
+  const Level& L = R.lev[l];
+  if (l == R.nc) {
+    MarchArgs a = march_args(h, R, x);
     a.out0 = y;
     launch_march<StApply<false>, false>(h, a);
     return;
   }
-  with_op(h, l, [&](auto op) {
+  with_op(R, l, [&](auto op) {
     k_apply<decltype(op), false><<<node_grid(L.g), node_block(), 0, h->stream>>>(
         op, L.g, x, y, nullptr, nullptr, kRedNone, nullptr, nullptr, nullptr);
   });
@@ -277,32 +634,31 @@ void apply_level(H* h, int l, const double2* x, double2* y) {
   h->count();
 }
 
-// y = A x and out = x.y (reduction op `rop` updates the PCG scalars)
-void apply_dot_fine(H* h, const double2* x, double2* y, RedOp rop, double* out) {
-  MarchArgs a = march_args(h, x);
-  a.out0 = y;
-  a.rop = rop;
-  a.red_out = out;
-  launch_march<StApply<true>, true>(h, a);
+// y = A x and x.y on every rank (reduction op `op` updates the PCG scalars)
+void apply_dot_fine(H* h, const std::function<const double2*(Rank&)>& x,
+                    const std::function<double2*(Rank&)>& y, RedOp op, bool want_out) {
+  reduce(
+      h, op,
+      [&](Rank& R, RedOp rop, double* out) {
+        MarchArgs a = march_args(h, R, x(R));
+        a.out0 = y(R);
+        a.rop = rop;
+        a.red_out = out;
+        launch_march<StApply<true>, true>(h, a);
+      },
+      want_out);
 }
 
-// one damped-Jacobi sweep; at the finest level optionally fused with z.r
-void sweep_level(H* h, int l, bool zero, const double2* xin, double2* xout, const double2* f,
-                 RedOp rop = kRedNone) {
-  const Level& L = h->lev[l];
-  if (l == h->nc && !zero) {
-    MarchArgs a = march_args(h, xin);
+void sweep_level(H* h, Rank& R, int l, bool zero, const double2* xin, double2* xout, const double2* f) {
+  const Level& L = R.lev[l];
+  if (l == R.nc && !zero) {
+    MarchArgs a = march_args(h, R, xin);
     a.f = f;
     a.out0 = xout;
-    if (rop != kRedNone) {
-      a.rop = rop;
-      launch_march<StSweep<true>, true>(h, a);
-    } else {
-      launch_march<StSweep<false>, false>(h, a);
-    }
+    launch_march<StSweep<false>, false>(h, a);
     return;
   }
-  with_op(h, l, [&](auto op) {
+  with_op(R, l, [&](auto op) {
     if (zero)
       k_sweep<decltype(op), true><<<node_grid(L.g), node_block(), 0, h->stream>>>(op, L.g, xin, xout, f, h->omega);
     else
@@ -312,124 +668,172 @@ void sweep_level(H* h, int l, bool zero, const double2* xin, double2* xout, cons
   h->count();
 }
 
-void residual_level(H* h, int l, const double2* x, const double2* f, double2* r) {
-  const Level& L = h->lev[l];
-  if (l == h->nc) {
-    MarchArgs a = march_args(h, x);
+void residual_level(H* h, Rank& R, int l, const double2* x, const double2* f, double2* r) {
+  const Level& L = R.lev[l];
+  if (l == R.nc) {
+    MarchArgs a = march_args(h, R, x);
     a.f = f;
     a.out0 = r;
     launch_march<StResidual, false>(h, a);
     return;
   }
-  with_op(h, l, [&](auto op) {
+  with_op(R, l, [&](auto op) {
     k_residual<decltype(op)><<<node_grid(L.g), node_block(), 0, h->stream>>>(op, L.g, x, f, r);
   });
   CKL();
   h->count();
 }
 
-void restrict_level(H* h, int l, const double2* r, double2* fc) {
-  k_restrict<<<node_grid(h->lev[l - 1].g), node_block(), 0, h->stream>>>(h->lev[l - 1].g, h->lev[l].g, r, fc);
+void restrict_level(H* h, Rank& R, int l, const double2* r, double2* fc) {
+  long off;
+  const Grid cg = coarse_of(h, R, l, off);
+  k_restrict<<<node_grid(cg), node_block(), 0, h->stream>>>(cg, R.lev[l].g, r, fc + off);
   CKL();
   h->count();
 }
 
-void prolong_level(H* h, int l, const double2* uc, double2* x, bool add) {
-  const Grid& fg = h->lev[l].g;
-  if (add) k_prolong<true><<<node_grid(fg), node_block(), 0, h->stream>>>(fg, h->lev[l - 1].g, uc, x);
-  else k_prolong<false><<<node_grid(fg), node_block(), 0, h->stream>>>(fg, h->lev[l - 1].g, uc, x);
+void prolong_level(H* h, Rank& R, int l, const double2* uc, double2* x, bool add) {
+  long off;
+  const Grid cg = coarse_of(h, R, l, off);
+  const Grid& fg = R.lev[l].g;
+  if (add) k_prolong<true><<<node_grid(fg), node_block(), 0, h->stream>>>(fg, cg, uc + off, x);
+  else k_prolong<false><<<node_grid(fg), node_block(), 0, h->stream>>>(fg, cg, uc + off, x);
   CKL();
   h->count();
 }
 
-void coarse_solve(H* h, const double2* f, double2* u) {
-  const int nodes = h->n0 / 2;
+void coarse_solve(H* h, Rank& R, const double2* f, double2* u) {
+  const int nodes = R.n0 / 2;
   const int nt = 256;
-  k_coarse_solve<<<(nodes + nt - 1) / nt, nt, sizeof(double) * h->n0, h->stream>>>(h->Ainv, h->n0, h->lev[0].g, f, u);
+  k_coarse_solve<<<(nodes + nt - 1) / nt, nt, sizeof(double) * R.n0, h->stream>>>(R.Ainv, R.n0, R.lev[0].g, f, u);
   CKL();
   h->count();
 }
 
-// One gamma-cycle at level l (mg_cycle, solvers.cpp:483-514). `zero` means
-// the iterate is logically zero on entry (the reference zeroes u_coarse
-// before the first visit, solvers.cpp:501, and pcgmg starts from z = 0,
-// solvers.cpp:524); the buffer content is then never read. At the finest
-// level the passes are the fused marching stages (tmg_march.cuh); when
-// `zr_op` is set the last post-sweep also reduces z.r for PCG. Returns
-// whether that reduction was fused.
+// One gamma-cycle at level l on every rank in lockstep (mg_cycle,
+// solvers.cpp:483-514). `zero` means the iterate is logically zero on entry
+// (the reference zeroes u_coarse before the first visit, solvers.cpp:501, and
+// pcgmg starts from z = 0, solvers.cpp:524); its buffer is then never read. At
+// the finest level the passes are the fused marching stages (tmg_march.cuh);
+// with `zr_op` set the last post-sweep also reduces z.r for PCG. Returns
+// whether that reduction was fused. Distributed levels exchange one ghost
+// column (two before the fused restriction) before every pass that reads
+// neighbours; the finest replicated level is assembled from the ranks' owned
+// columns after the restriction.
 bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp zr_op = kRedNone) {
-  Level& L = h->lev[l];
+  auto& rs = h->ranks;
   if (l == 0) {
-    coarse_solve(h, L.f, L.u[L.cur]);
+    for (Rank* R : rs) coarse_solve(h, *R, R->lev[0].f, R->lev[0].u[R->lev[0].cur]);
     return false;
   }
-  Level& C = h->lev[l - 1];
   const bool fine = (l == h->nc);
+  const bool dist = h->dist(l);
+  const bool cdist = h->dist(l - 1);
+  auto cur = [&](Rank& R) { return R.lev[l].u[R.lev[l].cur]; };
+  auto nxt = [&](Rank& R) { return R.lev[l].u[R.lev[l].cur ^ 1]; };
+  auto flip = [&] {
+    for (Rank* R : rs) R->lev[l].cur ^= 1;
+  };
   int s = 0;
   if (fine && zero && pre >= 2) {
-    MarchArgs a = march_args(h, nullptr);
-    a.f = L.f;
-    a.out0 = L.u[L.cur ^ 1];
-    launch_march<StSweep01, false>(h, a);
-    L.cur ^= 1;
+    // the finest f (the PCG residual) already carries its halo
+    for (Rank* R : rs) {
+      MarchArgs a = march_args(h, *R, nullptr);
+      a.f = R->lev[l].f;
+      a.out0 = nxt(*R);
+      launch_march<StSweep01, false>(h, a);
+    }
+    flip();
     s = 2;
     zero = false;
   }
   for (; s < pre; ++s) {
-    sweep_level(h, l, zero, L.u[L.cur], L.u[L.cur ^ 1], L.f);
-    L.cur ^= 1;
+    if (!zero) halo_vec(h, l, cur);
+    for (Rank* R : rs) sweep_level(h, *R, l, zero, cur(*R), nxt(*R), R->lev[l].f);
+    flip();
     zero = false;
   }
   if (zero) {
-    restrict_level(h, l, L.f, C.f);  // residual of u = 0 is f
+    halo_vec(h, l, [&](Rank& R) { return R.lev[l].f; });
+    for (Rank* R : rs) restrict_level(h, *R, l, R->lev[l].f, R->lev[l - 1].f);
   } else if (fine) {
-    MarchArgs a = march_args(h, L.u[L.cur]);
-    a.f = L.f;
-    a.out0 = C.f;
-    launch_march<StResidRestrict, false>(h, a);
+    halo_vec(h, l, cur, 2, 1);
+    for (Rank* R : rs) {
+      MarchArgs a = march_args(h, *R, cur(*R));
+      long coff;
+      a.gc = coarse_of(h, *R, l, coff);
+      a.f = R->lev[l].f;
+      a.out0 = R->lev[l - 1].f + coff;
+      launch_march<StResidRestrict, false>(h, a);
+    }
   } else {
-    residual_level(h, l, L.u[L.cur], L.f, L.res);
-    restrict_level(h, l, L.res, C.f);
+    halo_vec(h, l, cur);
+    for (Rank* R : rs) residual_level(h, *R, l, cur(*R), R->lev[l].f, R->lev[l].res);
+    halo_vec(h, l, [&](Rank& R) { return R.lev[l].res; });
+    for (Rank* R : rs) restrict_level(h, *R, l, R->lev[l].res, R->lev[l - 1].f);
   }
+  if (dist && !cdist) gather_level(h, l - 1, [&](Rank& R) -> void* { return R.lev[l - 1].f; }, sizeof(double2), 0, 1);
   const int visits = fine ? 1 : gamma;
   for (int t = 0; t < visits; ++t) enqueue_cycle(h, l - 1, t == 0, gamma, pre, post);
+  auto ccur = [&](Rank& R) { return R.lev[l - 1].u[R.lev[l - 1].cur]; };
+  if (cdist) halo_vec(h, l - 1, ccur);
   int p = 0;
   if (fine && !zero && post >= 1) {
-    MarchArgs a = march_args(h, L.u[L.cur]);
-    a.uc = C.u[C.cur];
-    a.f = L.f;
-    a.out0 = L.u[L.cur ^ 1];
-    launch_march<StProlongSweep, false>(h, a);
-    L.cur ^= 1;
+    for (Rank* R : rs) {
+      MarchArgs a = march_args(h, *R, cur(*R));
+      long coff;
+      a.gc = coarse_of(h, *R, l, coff);
+      a.uc = ccur(*R) + coff;
+      a.f = R->lev[l].f;
+      a.out0 = nxt(*R);
+      launch_march<StProlongSweep, false>(h, a);
+    }
+    flip();
     p = 1;
   } else {
-    prolong_level(h, l, C.u[C.cur], L.u[L.cur], !zero);
+    for (Rank* R : rs) prolong_level(h, *R, l, ccur(*R), cur(*R), !zero);
   }
   bool fused = false;
   for (; p < post; ++p) {
+    halo_vec(h, l, cur);
     const bool last = (p == post - 1);
-    sweep_level(h, l, false, L.u[L.cur], L.u[L.cur ^ 1], L.f, (fine && last) ? zr_op : kRedNone);
-    fused = fine && last && zr_op != kRedNone;
-    L.cur ^= 1;
+    if (fine && last && zr_op != kRedNone) {
+      reduce(h, zr_op, [&](Rank& R, RedOp rop, double* out) {
+        MarchArgs a = march_args(h, R, cur(R));
+        a.f = R.lev[l].f;
+        a.out0 = nxt(R);
+        a.rop = rop;
+        a.red_out = out;
+        launch_march<StSweep<true>, true>(h, a);
+      });
+      fused = true;
+    } else {
+      for (Rank* R : rs) sweep_level(h, *R, l, false, cur(*R), nxt(*R), R->lev[l].f);
+    }
+    flip();
   }
   return fused;
 }
-
-long flat2(const Level& L) { return L.g.size; }  // double2 count of a padded field
 
 int red_grid(long n2) {
   long b = (n2 + kRedThreads - 1) / kRedThreads;
   return static_cast<int>(b < kRedBlocks ? (b < 1 ? 1 : b) : kRedBlocks);
 }
 
-void dot(H* h, const double2* a, const double2* b, RedOp op, double* out) {
-  // owned columns only: ghost columns may hold a neighbour's halo
-  const Grid& g = h->fine().g;
-  const long o = g.own_begin(), n2 = g.own_count();
-  k_dot<<<red_grid(n2), kRedThreads, 0, h->stream>>>(a + o, b + o, n2, h->partials, h->ticket, op, h->st,
-                                                     h->hm_dev, out);
-  CKL();
-  h->count();
+// a.b over the owned columns of the finest level of every rank
+void dot(H* h, const std::function<const double2*(Rank&)>& a, const std::function<const double2*(Rank&)>& b,
+         RedOp op, bool want_out) {
+  reduce(
+      h, op,
+      [&](Rank& R, RedOp rop, double* out) {
+        const Grid& g = R.fine().g;
+        const long o = g.own_begin(), n2 = g.own_count();
+        k_dot<<<red_grid(n2), kRedThreads, 0, h->stream>>>(a(R) + o, b(R) + o, n2, R.partials, R.ticket, rop, R.st,
+                                                           R.hm_dev, out);
+        CKL();
+        h->count();
+      },
+      want_out);
 }
 
 // One PCG iteration (pcg_solve loop body, solvers.cpp:359-391) as a graph.
@@ -441,34 +845,41 @@ void capture_iteration(H* h, int gamma, int pre, int post) {
     if (gx) cudaGraphExecDestroy(gx);
     gx = nullptr;
   }
-  const long n2 = flat2(h->fine());
+  const int nc = h->nc;
   for (int k = 0; k < 2; ++k) {
-    for (Level& L : h->lev) L.cur = 0;
-    double2* p_old = h->pbuf[k];
-    double2* p_new = h->pbuf[k ^ 1];
+    for (Rank* R : h->ranks)
+      for (Level& L : R->lev) L.cur = 0;
     cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
     h->capturing = true;
     h->capture_kernels = 0;
     try {
       // z = M^-1 r: one cycle from z = 0 (solvers.cpp:523-527), fused with z.r
-      const bool fused = enqueue_cycle(h, h->nc, true, gamma, pre, post, kRedZr);
-      double2* z = h->fine().u[h->fine().cur];
-      if (!fused) dot(h, z, h->r, kRedZr, nullptr);
+      const bool fused = enqueue_cycle(h, nc, true, gamma, pre, post, kRedZr);
+      auto z = [&](Rank& R) { return R.fine().u[R.fine().cur]; };
+      if (!fused) dot(h, z, [&](Rank& R) { return R.r; }, kRedZr, false);
       // p = z + beta p; Ap; pAp; alpha (solvers.cpp:367-382)
-      MarchArgs a = march_args(h, z);
-      a.u2 = p_old;
-      a.out0 = p_new;
-      a.out1 = h->ap;
-      a.rop = kRedPap;
-      launch_march<StPupd, true>(h, a);
+      halo_vec(h, nc, z);
+      reduce(h, kRedPap, [&](Rank& R, RedOp rop, double* out) {
+        MarchArgs a = march_args(h, R, z(R));
+        a.u2 = R.pbuf[k];
+        a.out0 = R.pbuf[k ^ 1];
+        a.out1 = R.ap;
+        a.rop = rop;
+        a.red_out = out;
+        launch_march<StPupd, true>(h, a);
+      });
+      halo_vec(h, nc, [&](Rank& R) { return R.pbuf[k ^ 1]; });
       // x += alpha p; r -= alpha Ap; rr (solvers.cpp:383-386)
-      const long o = h->fine().g.own_begin(), no = h->fine().g.own_count();
-      k_update_xr<<<red_grid(no), kRedThreads, 0, h->stream>>>(h->x + o, h->r + o, p_new + o, h->ap + o, no,
-                                                                 h->partials,
-                                                                 h->ticket, h->st, h->hm_dev);
-      CKL();
-      h->count();
+      reduce(h, kRedRr, [&](Rank& R, RedOp rop, double* out) {
+        const long o = R.fine().g.own_begin(), no = R.fine().g.own_count();
+        k_update_xr<<<red_grid(no), kRedThreads, 0, h->stream>>>(R.x + o, R.r + o, R.pbuf[k ^ 1] + o, R.ap + o,
+                                                                   no, R.partials, R.ticket, rop, R.st, R.hm_dev,
+                                                                   out);
+        CKL();
+        h->count();
+      });
+      halo_vec(h, nc, [&](Rank& R) { return R.r; });
     } catch (...) {
       h->capturing = false;
       cudaStreamEndCapture(h->stream, &g);
@@ -495,40 +906,64 @@ void setup(H* h, double omega) {
   h->have_setup = false;
   // Galerkin hierarchy, finest to coarsest (solvers.cpp:474-478)
   for (int l = h->nc; l >= 1; --l) {
-    const Grid& cg = h->lev[l - 1].g;
-    dim3 blk(32, 4), grd((cg.ny + 1 + 31) / 32, (cg.nx + 1 + 3) / 4);
-    with_op(h, l, [&](auto op) {
-      k_galerkin<decltype(op)><<<grd, blk, 0, h->stream>>>(op, h->lev[l].g, cg, h->lev[l - 1].S, cg.size);
+    for (Rank* R : h->ranks) {
+      long off;
+      const Grid cg = coarse_of(h, *R, l, off);
+      dim3 blk(32, 4), grd((cg.ny + 1 + 31) / 32, (cg.ncol + 3) / 4);
+      // the output pointer is offset by `off` nodes inside every plane; the
+      // plane stride stays that of the stored level
+      with_op(*R, l, [&](auto op) {
+        k_galerkin<decltype(op)><<<grd, blk, 0, h->stream>>>(op, R->lev[l].g, cg, R->lev[l - 1].S + off,
+                                                             R->lev[l - 1].g.size);
+      });
+      CKL();
+      h->count();
+    }
+    if (h->dist(l - 1)) {
+      // ghost columns of the new level's stencil (backward blocks, Galerkin
+      // of the next level reads two columns to the left)
+      for (int k = 0; k < kStencilPlanes; ++k)
+        h->comm->halo(h->ranks, l - 1,
+                      [&](Rank& R) -> void* { return R.lev[l - 1].S + static_cast<long>(k) * R.lev[l - 1].g.size; },
+                      sizeof(double), kGX, 1, h->stream);
+    } else if (h->dist(l)) {
+      gather_level(h, l - 1, [&](Rank& R) -> void* { return R.lev[l - 1].S; }, sizeof(double),
+                   h->ranks[0]->lev[l - 1].g.size, kStencilPlanes);
+    }
+  }
+  // coarsest: dense matrix -> Cholesky -> explicit symmetric inverse (replicated)
+  for (Rank* R : h->ranks) {
+    const int n = R->n0;
+    const Grid& g0 = R->lev[0].g;
+    CK(cudaMemsetAsync(R->A0, 0, sizeof(double) * n * n, h->stream));
+    with_op(*R, 0, [&](auto op) {
+      k_dense_assemble<decltype(op)><<<dim3((g0.ny + 1 + 63) / 64, g0.nx + 1), 64, 0, h->stream>>>(op, g0, R->A0, n);
     });
     CKL();
-    h->count();
+    k_cholesky<<<1, 1024, 0, h->stream>>>(R->A0, n, R->bad_row);
+    CKL();
+    h->count(2);
   }
-  // coarsest: dense matrix -> Cholesky -> explicit symmetric inverse
-  const int n = h->n0;
-  const Grid& g0 = h->lev[0].g;
-  CK(cudaMemsetAsync(h->A0, 0, sizeof(double) * n * n, h->stream));
-  with_op(h, 0, [&](auto op) {
-    k_dense_assemble<decltype(op)><<<dim3((g0.ny + 1 + 63) / 64, g0.nx + 1), 64, 0, h->stream>>>(op, g0, h->A0, n);
-  });
-  CKL();
-  k_cholesky<<<1, 1024, 0, h->stream>>>(h->A0, n, h->bad_row);
-  CKL();
-  int bad = -1;
-  CK(cudaMemcpyAsync(&bad, h->bad_row, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaStreamSynchronize(h->stream));
-  h->count(3);
-  if (bad >= 0) {
-    fail(TMG_ERR_DEFINITENESS,
-         "matrix is not positive definite: non-positive pivot at row " + std::to_string(bad), bad);
+  for (Rank* R : h->ranks) {
+    int bad = -1;
+    CK(cudaMemcpyAsync(&bad, R->bad_row, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (bad >= 0) {
+      fail(TMG_ERR_DEFINITENESS,
+           "matrix is not positive definite: non-positive pivot at row " + std::to_string(bad), bad);
+    }
   }
-  const int wpb = 4;
-  const size_t sm = sizeof(double) * n * wpb;
-  CK(cudaFuncSetAttribute(k_lower_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-  k_lower_inverse<<<(n + wpb - 1) / wpb, 32 * wpb, sm, h->stream>>>(h->A0, h->LiT, n);
-  CKL();
-  k_gram<<<dim3((n + 127) / 128, n), 128, 0, h->stream>>>(h->LiT, h->Ainv, n);
-  CKL();
-  h->count(2);
+  for (Rank* R : h->ranks) {
+    const int n = R->n0;
+    const int wpb = 4;
+    const size_t sm = sizeof(double) * n * wpb;
+    CK(cudaFuncSetAttribute(k_lower_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    k_lower_inverse<<<(n + wpb - 1) / wpb, 32 * wpb, sm, h->stream>>>(R->A0, R->LiT, n);
+    CKL();
+    k_gram<<<dim3((n + 127) / 128, n), 128, 0, h->stream>>>(R->LiT, R->Ainv, n);
+    CKL();
+    h->count(2);
+  }
   h->have_setup = true;
 }
 
@@ -542,8 +977,7 @@ struct SolveOut {
   std::vector<double> hist;
 };
 
-void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int pre, int post,
-                    SolveOut& o) {
+void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int pre, int post, SolveOut& o) {
   need_setup(h);
   // SolverConfig::validate subset enforced by pcgmg_solve (solvers.cpp:518-521)
   if (pre != post) {
@@ -551,41 +985,50 @@ void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int 
   }
   if (gamma != 1 && gamma != 2) fail(TMG_ERR_CONFIG, "gamma must be 1 (V-cycle) or 2 (W-cycle)");
   if (pre < 0) fail(TMG_ERR_CONFIG, "smoothing sweep counts must be non-negative");
-  const Level& F = h->fine();
-  const long n2 = flat2(F);
+  const int nc = h->nc;
   capture_iteration(h, gamma, pre, post);
   CK(cudaEventRecord(h->ev[0], h->stream));
-  dot(h, h->b, h->b, kRedB, nullptr);
-  k_pcg_begin<<<1, 1, 0, h->stream>>>(h->st);
-  CKL();
-  h->count();
-  CK(cudaMemsetAsync(h->pbuf[0], 0, sizeof(double2) * n2, h->stream));
-  if (use_x0) {
-    CK(cudaMemcpyAsync(h->x, h->x0, sizeof(double2) * n2, cudaMemcpyDeviceToDevice, h->stream));
-    apply_level(h, h->nc, h->x, F.res);
-    k_sub<<<red_grid(F.g.own_count()), kRedThreads, 0, h->stream>>>(h->b + F.g.own_begin(), F.res + F.g.own_begin(),
-                                                                   h->r + F.g.own_begin(), F.g.own_count());
-  } else {
-    CK(cudaMemsetAsync(h->x, 0, sizeof(double2) * n2, h->stream));
-    k_sub<<<red_grid(F.g.own_count()), kRedThreads, 0, h->stream>>>(h->b + F.g.own_begin(), nullptr,
-                                                                   h->r + F.g.own_begin(), F.g.own_count());
+  auto bvec = [&](Rank& R) { return R.b; };
+  dot(h, bvec, bvec, kRedB, false);
+  for (Rank* R : h->ranks) {
+    k_pcg_begin<<<1, 1, 0, h->stream>>>(R->st);
+    CKL();
+    h->count();
+    const Level& F = R->fine();
+    const long n2 = F.g.size;
+    CK(cudaMemsetAsync(R->pbuf[0], 0, sizeof(double2) * n2, h->stream));
+    if (use_x0) CK(cudaMemcpyAsync(R->x, R->x0, sizeof(double2) * n2, cudaMemcpyDeviceToDevice, h->stream));
+    else CK(cudaMemsetAsync(R->x, 0, sizeof(double2) * n2, h->stream));
   }
-  CKL();
-  h->count();
-  dot(h, h->r, h->r, kRedPlain, h->scal);
+  if (use_x0) {
+    halo_vec(h, nc, [&](Rank& R) { return R.x; });
+    for (Rank* R : h->ranks) apply_level(h, *R, nc, R->x, R->fine().res);
+  }
+  for (Rank* R : h->ranks) {
+    const Grid& g = R->fine().g;
+    const long o = g.own_begin();
+    k_sub<<<red_grid(g.own_count()), kRedThreads, 0, h->stream>>>(R->b + o, use_x0 ? R->fine().res + o : nullptr,
+                                                                   R->r + o, g.own_count());
+    CKL();
+    h->count();
+  }
+  halo_vec(h, nc, [&](Rank& R) { return R.r; });
+  auto rvec = [&](Rank& R) { return R.r; };
+  dot(h, rvec, rvec, kRedPlain, true);
+  Rank& R0 = *h->ranks[0];
   PcgState st0;
-  CK(cudaMemcpyAsync(&st0, h->st, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaMemcpyAsync(h->scal_host, h->scal, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(&st0, R0.st, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaMemcpyAsync(R0.scal_host, R0.scal, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   o = SolveOut{};
   h->have_solution = true;
   // pcg_solve, solvers.cpp:336-357
   if (st0.bnorm == 0.0) {
-    CK(cudaMemsetAsync(h->x, 0, sizeof(double2) * n2, h->stream));
+    for (Rank* R : h->ranks) CK(cudaMemsetAsync(R->x, 0, sizeof(double2) * R->fine().g.size, h->stream));
     o.converged = 1;
     o.hist.push_back(0.0);
   } else {
-    double rel = std::sqrt(*h->scal_host) / st0.bnorm;
+    double rel = std::sqrt(*R0.scal_host) / st0.bnorm;
     o.final_residual = rel;
     o.hist.push_back(rel);
     if (rel <= tol) {
@@ -595,19 +1038,18 @@ void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int 
         CK(cudaGraphLaunch(h->graph[(it - 1) & 1], h->stream));
         h->launches += h->graph_kernels;
         CK(cudaStreamSynchronize(h->stream));
-        const volatile HostMirror* m = h->hm;
+        const volatile HostMirror* m = R0.hm;
         const int status = m->status;
         if (status == 4) {
           char buf[200];
-          std::snprintf(buf, sizeof buf,
-                        "preconditioner is not positive definite: z^T r = %f at iteration %d",
+          std::snprintf(buf, sizeof buf, "preconditioner is not positive definite: z^T r = %f at iteration %d",
                         static_cast<double>(m->zr), it);
           fail(TMG_ERR_PRECONDITIONER, buf);
         }
         if (status == 3) {
           char buf[200];
-          std::snprintf(buf, sizeof buf, "PCG breakdown: p^T A p = %f at iteration %d",
-                        static_cast<double>(m->pap), it);
+          std::snprintf(buf, sizeof buf, "PCG breakdown: p^T A p = %f at iteration %d", static_cast<double>(m->pap),
+                        it);
           fail(TMG_ERR_DEFINITENESS, buf);
         }
         rel = m->relres;
@@ -641,6 +1083,7 @@ template <class F>
 int guarded(H* h, F&& fn) {
   if (!h) return TMG_ERR_DIMENSION;
   try {
+    if (!h->stream) fail(TMG_ERR_CUDA, h->err.empty() ? "handle has no device" : h->err);
     CK(cudaSetDevice(h->device));
     fn();
     h->err.clear();
@@ -660,120 +1103,147 @@ void copy_out_hist(const SolveOut& o, double* history, int cap, int* len) {
   if (len) *len = m;
 }
 
-}  // namespace
+// Host upload of the fine moduli of one rank: element columns
+// [x0 - kGX, x0 + ncol + kGX) clipped to the mesh (ghost elements stay 0).
+void upload_moduli_rank(H* h, Rank& R, const double* moduli) {
+  const Grid& g = R.fine().g;
+  const int e0 = std::max(0, g.x0 - kGX), e1 = std::min(g.nx, g.x0 + g.ncol + kGX);
+  if (e1 > e0)
+    CK(cudaMemcpy2DAsync(R.E + g.idx(e0 - g.x0, 0), sizeof(double) * g.P, moduli + static_cast<long>(e0) * g.ny,
+                         sizeof(double) * g.ny, sizeof(double) * g.ny, e1 - e0, cudaMemcpyHostToDevice, h->stream));
+}
 
-// =================================================================== ABI ==
-
-extern "C" {
-
-int tmg_gpu_create(int nx, int ny, int num_coarsenings, int dofs_per_node, int device,
-                   tmg_gpu_handle** out) {
-  if (!out) return TMG_ERR_DIMENSION;
-  *out = nullptr;
+int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks, int rank, int nlocal,
+                  const void* nccl_id, int rep) {
   // build_hierarchy validation (grid.cpp:55-80)
-  auto h = std::make_unique<tmg_gpu_handle>();
-  h->device = device;
   auto cfg = [&](const std::string& m) {
-    h->err = m;
-    *out = h.release();
+    hp->err = m;
     return TMG_ERR_CONFIG;
   };
   if (nx < 1 || ny < 1)
-    return cfg("grid must have at least one element per direction, got " + std::to_string(nx) +
-               "x" + std::to_string(ny));
-  if (num_coarsenings < 0) return cfg("num_coarsenings must be non-negative");
-  if (dofs_per_node != 2)
-    return cfg("dofs_per_node must be 2: the GPU path solves the plane-elasticity system");
-  if (num_coarsenings > 24) return cfg("num_coarsenings too large");
-  const int factor = 1 << num_coarsenings;
+    return cfg("grid must have at least one element per direction, got " + std::to_string(nx) + "x" +
+               std::to_string(ny));
+  if (nc < 0) return cfg("num_coarsenings must be non-negative");
+  if (dpn != 2) return cfg("dofs_per_node must be 2: the GPU path solves the plane-elasticity system");
+  if (nc > 24) return cfg("num_coarsenings too large");
+  const int factor = 1 << nc;
   if (nx % factor != 0)
-    return cfg("nx = " + std::to_string(nx) + " is not divisible by 2^" +
-               std::to_string(num_coarsenings) + " = " + std::to_string(factor));
+    return cfg("nx = " + std::to_string(nx) + " is not divisible by 2^" + std::to_string(nc) + " = " +
+               std::to_string(factor));
   if (ny % factor != 0)
-    return cfg("ny = " + std::to_string(ny) + " is not divisible by 2^" +
-               std::to_string(num_coarsenings) + " = " + std::to_string(factor));
+    return cfg("ny = " + std::to_string(ny) + " is not divisible by 2^" + std::to_string(nc) + " = " +
+               std::to_string(factor));
   const int n0 = 2 * (nx / factor + 1) * (ny / factor + 1);
   if (n0 > 2048) {
     return cfg("coarsest level has " + std::to_string(n0) +
                " dofs; the device coarse solve supports <= 2048 (add coarsenings)");
   }
-  H* hp = h.get();
-  const int st = guarded(hp, [&] {
-    int ndev = 0;
-    CK(cudaGetDeviceCount(&ndev));
-    if (device < 0 || device >= ndev) fail(TMG_ERR_CUDA, "CUDA device " + std::to_string(device) + " not present");
-    cudaDeviceProp prop;
-    CK(cudaGetDeviceProperties(&prop, device));
-    if (prop.major != 10) {
-      fail(TMG_ERR_CUDA, std::string("libtmg_gpu is built for sm_100a; device is ") + prop.name);
-    }
-    CK(cudaSetDevice(device));
-    CK(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking));
-    for (cudaEvent_t& e : hp->ev) CK(cudaEventCreate(&e));
-    hp->nx = nx;
-    hp->ny = ny;
-    hp->nc = num_coarsenings;
-    hp->lev.resize(num_coarsenings + 1);
-    for (int l = 0; l <= num_coarsenings; ++l) {
-      Level& L = hp->lev[l];
-      const int s = 1 << (num_coarsenings - l);
-      L.g = make_grid(nx / s, ny / s);
-      L.ndof = 2L * (L.g.nx + 1) * (L.g.ny + 1);
-      const size_t vb = sizeof(double2) * (L.g.size + kSlackNodes);
-      CK(cudaMalloc(&L.u[0], vb));
-      CK(cudaMalloc(&L.u[1], vb));
-      CK(cudaMalloc(&L.res, vb));
-      CK(cudaMemsetAsync(L.u[0], 0, vb, hp->stream));
-      CK(cudaMemsetAsync(L.u[1], 0, vb, hp->stream));
-      CK(cudaMemsetAsync(L.res, 0, vb, hp->stream));
-      if (l < num_coarsenings) {
-        CK(cudaMalloc(&L.f, vb));
-        CK(cudaMemsetAsync(L.f, 0, vb, hp->stream));
-        const size_t sb = sizeof(double) * kStencilPlanes * L.g.size;
-        CK(cudaMalloc(&L.S, sb));
-        CK(cudaMemsetAsync(L.S, 0, sb, hp->stream));
-      }
-    }
-    Level& F = hp->fine();
-    const size_t vb = sizeof(double2) * (F.g.size + kSlackNodes);
-    for (double2** v : {&hp->x, &hp->r, &hp->pbuf[0], &hp->pbuf[1], &hp->ap, &hp->b, &hp->x0}) {
-      CK(cudaMalloc(v, vb));
-      CK(cudaMemsetAsync(*v, 0, vb, hp->stream));
-    }
-    F.f = hp->r;  // the finest cycle smooths against the PCG residual
-    CK(cudaMalloc(&hp->E, sizeof(double) * (F.g.size + kSlackNodes)));
-    CK(cudaMemsetAsync(hp->E, 0, sizeof(double) * (F.g.size + kSlackNodes), hp->stream));
-    CK(cudaMalloc(&hp->M, F.g.size + kSlackNodes));
-    CK(cudaMemsetAsync(hp->M, 0, F.g.size + kSlackNodes, hp->stream));
-    hp->n0 = n0;
-    CK(cudaMalloc(&hp->A0, sizeof(double) * n0 * n0));
-    CK(cudaMalloc(&hp->LiT, sizeof(double) * n0 * n0));
-    CK(cudaMalloc(&hp->Ainv, sizeof(double) * n0 * n0));
-    CK(cudaMalloc(&hp->bad_row, sizeof(int)));
-    const dim3 ng = node_grid(F.g);
-    const long nparts = std::max<long>(static_cast<long>(ng.x) * ng.y, kRedBlocks);
-    CK(cudaMalloc(&hp->partials, sizeof(double) * nparts));
-    CK(cudaMalloc(&hp->ticket, sizeof(unsigned)));
-    CK(cudaMemsetAsync(hp->ticket, 0, sizeof(unsigned), hp->stream));
-    CK(cudaMalloc(&hp->st, sizeof(PcgState)));
-    CK(cudaMemsetAsync(hp->st, 0, sizeof(PcgState), hp->stream));
-    CK(cudaMalloc(&hp->scal, sizeof(double)));
-    CK(cudaHostAlloc(&hp->hm, sizeof(HostMirror), cudaHostAllocMapped));
-    std::memset(hp->hm, 0, sizeof(HostMirror));
-    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hp->hm_dev), hp->hm, 0));
-    CK(cudaHostAlloc(&hp->scal_host, sizeof(double), cudaHostAllocDefault));
-    CK(cudaStreamSynchronize(hp->stream));
-  });
-  if (st != TMG_OK) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) return cfg("invalid rank / nranks");
+  hp->device = device;
+  hp->nx = nx;
+  hp->ny = ny;
+  hp->nc = nc;
+  hp->nranks = nranks;
+  hp->rep = (nranks == 1) ? nc : (rep >= 0 ? std::min(rep, nc - 1) : auto_rep(nx, nc, nranks));
+  if (nranks > 1) {
+    if (nc < 1 || hp->rep >= nc) return cfg("a distributed solve needs at least the finest level distributed");
+    hp->xpart = partition(nx, nc, hp->rep, nranks);
+    for (int r = 0; r < nranks; ++r)
+      if (hp->xpart[r + 1] - hp->xpart[r] < (2 << (nc - hp->rep)))
+        return cfg("mesh too small for " + std::to_string(nranks) + " slabs");
+  } else {
+    hp->xpart = {0, nx + 1};
+  }
+  hp->stream = nullptr;
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) fail(TMG_ERR_CUDA, "CUDA device " + std::to_string(device) + " not present");
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) fail(TMG_ERR_CUDA, std::string("libtmg_gpu is built for sm_100a; device is ") + prop.name);
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : hp->ev) CK(cudaEventCreate(&e));
+  for (int i = 0; i < nlocal; ++i) {
+    hp->own.push_back(std::make_unique<Rank>());
+    Rank& R = *hp->own.back();
+    R.index = (nlocal == 1) ? rank : i;
+    hp->ranks.push_back(&R);
+    alloc_rank(hp, R);
+  }
+  if (nranks > 1) {
+    if (nlocal > 1) hp->comm = std::make_unique<LocalComm>(hp->ranks);
+    else hp->comm = std::make_unique<NcclComm>(nranks, rank, nccl_id);
+  }
+  CK(cudaStreamSynchronize(hp->stream));
+  return TMG_OK;
+}
+
+int create_handle(int nx, int ny, int nc, int dpn, int device, int nranks, int rank, int nlocal, const void* id,
+                  int rep, tmg_gpu_handle** out) {
+  if (!out) return TMG_ERR_DIMENSION;
+  auto h = std::make_unique<tmg_gpu_handle>();
+  h->device = device;
+  int st = TMG_OK;
+  try {
+    st = create_common(h.get(), nx, ny, nc, dpn, device, nranks, rank, nlocal, id, rep);
+  } catch (const TmgError& e) {
+    st = finish(h.get(), e);
+  }
+  if (st != TMG_OK && h->stream) {
     // keep only the message: the caller may read it, then destroys the handle
-    const std::string msg = hp->err;
-    free_handle(hp);
+    const std::string msg = h->err;
+    free_handle(h.get());
     h = std::make_unique<tmg_gpu_handle>();
     h->device = device;
     h->err = msg;
   }
   *out = h.release();
   return st;
+}
+
+}  // namespace
+
+// =================================================================== ABI ==
+
+extern "C" {
+
+int tmg_gpu_create(int nx, int ny, int num_coarsenings, int dofs_per_node, int device, tmg_gpu_handle** out) {
+  return create_handle(nx, ny, num_coarsenings, dofs_per_node, device, 1, 0, 1, nullptr, -1, out);
+}
+
+int tmg_gpu_create_local_slabs(int nx, int ny, int num_coarsenings, int dofs_per_node, int device, int nslabs,
+                               int replicated_level, tmg_gpu_handle** out) {
+  return create_handle(nx, ny, num_coarsenings, dofs_per_node, device, nslabs, 0, nslabs, nullptr,
+                       replicated_level, out);
+}
+
+int tmg_gpu_create_nccl(int nx, int ny, int num_coarsenings, int dofs_per_node, int device, int nranks, int rank,
+                        const void* nccl_unique_id, int replicated_level, tmg_gpu_handle** out) {
+  return create_handle(nx, ny, num_coarsenings, dofs_per_node, device, nranks, rank, 1, nccl_unique_id,
+                       replicated_level, out);
+}
+
+int tmg_nccl_unique_id(void* out128) {
+  try {
+    ncclUniqueId id;
+    NK(nccl().getUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+    return TMG_OK;
+  } catch (const TmgError& e) {
+    return e.code;
+  }
+}
+
+int tmg_partition(int nx, int num_coarsenings, int nranks, int replicated_level, int* x0s, int* rep_out) {
+  if (nranks < 1 || num_coarsenings < 0) return TMG_ERR_CONFIG;
+  const int rep = nranks == 1 ? num_coarsenings
+                              : (replicated_level >= 0 ? std::min(replicated_level, num_coarsenings - 1)
+                                                       : auto_rep(nx, num_coarsenings, nranks));
+  const std::vector<int> xp = nranks == 1 ? std::vector<int>{0, nx + 1} : partition(nx, num_coarsenings, rep, nranks);
+  std::memcpy(x0s, xp.data(), sizeof(int) * xp.size());
+  if (rep_out) *rep_out = rep;
+  return TMG_OK;
 }
 
 void tmg_gpu_destroy(tmg_gpu_handle* h) {
@@ -791,9 +1261,7 @@ int tmg_gpu_last_error(tmg_gpu_handle* h, char* buf, int len, int* row) {
 
 int tmg_gpu_set_problem(tmg_gpu_handle* h, double nu, const int* fixed_dofs, int n_fixed) {
   return guarded(h, [&] {
-    if (!h->stream) fail(TMG_ERR_CUDA, "handle has no device");
-    const Grid& g = h->fine().g;
-    const long ndof = h->fine().ndof;
+    const long ndof = 2L * (h->nx + 1) * (h->ny + 1);
     // BoundaryConditions::validate (fem.cpp:110-129)
     std::vector<int> cnt(ndof, 0);
     for (int k = 0; k < n_fixed; ++k) {
@@ -802,14 +1270,21 @@ int tmg_gpu_set_problem(tmg_gpu_handle* h, double nu, const int* fixed_dofs, int
         fail(TMG_ERR_CONFIG, "fixed dof " + std::to_string(d) + " outside [0, " + std::to_string(ndof) + ")");
       cnt[d]++;
     }
-    std::vector<uint8_t> mask(g.size, 0);
-    for (int x = 0; x <= g.nx; ++x)
-      for (int y = 0; y <= g.ny; ++y) {
-        const long node = static_cast<long>(x) * (g.ny + 1) + y;
-        const int c0 = std::min(cnt[2 * node], 15), c1 = std::min(cnt[2 * node + 1], 15);
-        mask[g.idx(x, y)] = static_cast<uint8_t>(c0 | (c1 << 4));
+    for (Rank* R : h->ranks) {
+      const Grid& g = R->fine().g;
+      std::vector<uint8_t> mask(g.size, 0);
+      for (int lx = -kGX; lx < g.ncol + kGX; ++lx) {
+        const int x = g.x0 + lx;
+        if (x < 0 || x > g.nx) continue;
+        for (int y = 0; y <= g.ny; ++y) {
+          const long node = static_cast<long>(x) * (g.ny + 1) + y;
+          const int c0 = std::min(cnt[2 * node], 15), c1 = std::min(cnt[2 * node + 1], 15);
+          mask[g.idx(lx, y)] = static_cast<uint8_t>(c0 | (c1 << 4));
+        }
       }
-    CK(cudaMemcpyAsync(h->M, mask.data(), g.size, cudaMemcpyHostToDevice, h->stream));
+      CK(cudaMemcpyAsync(R->M, mask.data(), g.size, cudaMemcpyHostToDevice, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+    }
     h->nu = nu;
     tmg_element_stiffness(1.0, nu, h->ke);
     CK(cudaMemcpyToSymbolAsync(c_k8, h->ke, 8 * sizeof(double), 0, cudaMemcpyHostToDevice, h->stream));  // row 0
@@ -822,13 +1297,10 @@ int tmg_gpu_set_problem(tmg_gpu_handle* h, double nu, const int* fixed_dofs, int
 
 int tmg_gpu_upload_moduli(tmg_gpu_handle* h, const double* moduli, long n_elem) {
   return guarded(h, [&] {
-    const Grid& g = h->fine().g;
-    if (n_elem != static_cast<long>(g.nx) * g.ny)
-      fail(TMG_ERR_DIMENSION, "element modulus count " + std::to_string(n_elem) +
-                                  " does not match grid with " +
-                                  std::to_string(static_cast<long>(g.nx) * g.ny) + " elements");
-    CK(cudaMemcpy2DAsync(h->E + g.idx(0, 0), sizeof(double) * g.P, moduli, sizeof(double) * g.ny,
-                         sizeof(double) * g.ny, g.nx, cudaMemcpyHostToDevice, h->stream));
+    if (n_elem != static_cast<long>(h->nx) * h->ny)
+      fail(TMG_ERR_DIMENSION, "element modulus count " + std::to_string(n_elem) + " does not match grid with " +
+                                  std::to_string(static_cast<long>(h->nx) * h->ny) + " elements");
+    for (Rank* R : h->ranks) upload_moduli_rank(h, *R, moduli);
     h->have_moduli = true;
     h->have_setup = false;
   });
@@ -852,16 +1324,18 @@ int tmg_gpu_set_moduli(tmg_gpu_handle* h, const double* moduli, long n_elem, dou
   return tmg_gpu_setup(h, omega);
 }
 
-int tmg_gpu_set_density(tmg_gpu_handle* h, const double* alpha, int nphases,
-                        const double* phase_moduli, double penalty, double omega) {
+int tmg_gpu_set_density(tmg_gpu_handle* h, const double* alpha, int nphases, const double* phase_moduli,
+                        double penalty, double omega) {
   const int s = guarded(h, [&] {
-    const Grid& g = h->fine().g;
+    need_single(h, "tmg_gpu_set_density");
+    Rank& R = *h->ranks[0];
+    const Grid& g = R.fine().g;
     const long ne = static_cast<long>(g.nx) * g.ny;
-    double* da = grow(h->aux, h->aux_cap, ne * nphases);
-    double* dp = grow(h->aux2, h->aux2_cap, nphases);
+    double* da = grow(R.aux, R.aux_cap, ne * nphases);
+    double* dp = grow(R.aux2, R.aux2_cap, nphases);
     CK(cudaMemcpyAsync(da, alpha, sizeof(double) * ne * nphases, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(dp, phase_moduli, sizeof(double) * nphases, cudaMemcpyHostToDevice, h->stream));
-    k_simp<<<dim3((g.ny + 127) / 128, g.nx), 128, 0, h->stream>>>(g, nphases, da, dp, penalty, h->E);
+    k_simp<<<dim3((g.ny + 127) / 128, g.nx), 128, 0, h->stream>>>(g, nphases, da, dp, penalty, R.E);
     CKL();
     h->count();
     h->have_moduli = true;
@@ -872,23 +1346,27 @@ int tmg_gpu_set_density(tmg_gpu_handle* h, const double* alpha, int nphases,
 }
 
 int tmg_gpu_upload_rhs(tmg_gpu_handle* h, const double* b) {
-  return guarded(h, [&] { upload_nodes(h, h->b, b, h->fine().g); });
+  return guarded(h, [&] {
+    for (Rank* R : h->ranks) upload_nodes(h->stream, R->b, b, R->fine().g);
+  });
 }
 
 int tmg_gpu_upload_x0(tmg_gpu_handle* h, const double* x0) {
-  return guarded(h, [&] { upload_nodes(h, h->x0, x0, h->fine().g); });
+  return guarded(h, [&] {
+    for (Rank* R : h->ranks) upload_nodes(h->stream, R->x0, x0, R->fine().g);
+  });
 }
 
 int tmg_gpu_solution_to_x0(tmg_gpu_handle* h) {
   return guarded(h, [&] {
-    CK(cudaMemcpyAsync(h->x0, h->x, sizeof(double2) * flat2(h->fine()), cudaMemcpyDeviceToDevice, h->stream));
+    for (Rank* R : h->ranks)
+      CK(cudaMemcpyAsync(R->x0, R->x, sizeof(double2) * R->fine().g.size, cudaMemcpyDeviceToDevice, h->stream));
   });
 }
 
-int tmg_gpu_solve_resident(tmg_gpu_handle* h, int use_x0, double tol, int max_iter, int gamma,
-                           int pre_sweeps, int post_sweeps, int* iterations, double* final_residual,
-                           int* converged, double* seconds, double* history, int history_cap,
-                           int* history_len) {
+int tmg_gpu_solve_resident(tmg_gpu_handle* h, int use_x0, double tol, int max_iter, int gamma, int pre_sweeps,
+                           int post_sweeps, int* iterations, double* final_residual, int* converged,
+                           double* seconds, double* history, int history_cap, int* history_len) {
   return guarded(h, [&] {
     SolveOut o;
     solve_resident(h, use_x0 != 0, tol, max_iter, gamma, pre_sweeps, post_sweeps, o);
@@ -901,20 +1379,25 @@ int tmg_gpu_solve_resident(tmg_gpu_handle* h, int use_x0, double tol, int max_it
 }
 
 int tmg_gpu_download_solution(tmg_gpu_handle* h, double* x_out) {
-  return guarded(h, [&] { download_nodes(h, x_out, h->x, h->fine().g); });
+  return guarded(h, [&] {
+    for (Rank* R : h->ranks) download_nodes(h->stream, x_out, R->x, R->fine().g);
+    CK(cudaStreamSynchronize(h->stream));
+  });
 }
 
-int tmg_gpu_solve(tmg_gpu_handle* h, const double* b, const double* x0, double tol, int max_iter,
-                  int gamma, int pre_sweeps, int post_sweeps, double* x_out, int* iterations,
-                  double* final_residual, int* converged, double* seconds, double* history,
-                  int history_cap, int* history_len) {
+int tmg_gpu_solve(tmg_gpu_handle* h, const double* b, const double* x0, double tol, int max_iter, int gamma,
+                  int pre_sweeps, int post_sweeps, double* x_out, int* iterations, double* final_residual,
+                  int* converged, double* seconds, double* history, int history_cap, int* history_len) {
   return guarded(h, [&] {
     need_setup(h);
-    upload_nodes(h, h->b, b, h->fine().g);
-    if (x0) upload_nodes(h, h->x0, x0, h->fine().g);
+    for (Rank* R : h->ranks) {
+      upload_nodes(h->stream, R->b, b, R->fine().g);
+      if (x0) upload_nodes(h->stream, R->x0, x0, R->fine().g);
+    }
     SolveOut o;
     solve_resident(h, x0 != nullptr, tol, max_iter, gamma, pre_sweeps, post_sweeps, o);
-    download_nodes(h, x_out, h->x, h->fine().g);
+    for (Rank* R : h->ranks) download_nodes(h->stream, x_out, R->x, R->fine().g);
+    CK(cudaStreamSynchronize(h->stream));
     if (iterations) *iterations = o.iterations;
     if (final_residual) *final_residual = o.final_residual;
     if (converged) *converged = o.converged;
@@ -926,35 +1409,35 @@ int tmg_gpu_solve(tmg_gpu_handle* h, const double* b, const double* x0, double t
 int tmg_gpu_compliance(tmg_gpu_handle* h, const double* u, double* out) {
   return guarded(h, [&] {
     if (!h->have_moduli || !h->have_problem) fail(TMG_ERR_DIMENSION, "operator not set");
-    Level& F = h->fine();
-    const double2* src = h->x;
-    if (u) {
-      upload_nodes(h, F.res, u, F.g);
-      src = F.res;
-    } else if (!h->have_solution) {
-      fail(TMG_ERR_DIMENSION, "no resident solution");
-    }
-    apply_dot_fine(h, src, F.u[1], kRedPlain, h->scal);
-    CK(cudaMemcpyAsync(h->scal_host, h->scal, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    if (!u && !h->have_solution) fail(TMG_ERR_DIMENSION, "no resident solution");
+    if (u)
+      for (Rank* R : h->ranks) upload_nodes(h->stream, R->fine().res, u, R->fine().g);
+    auto src = [&](Rank& R) -> double2* { return u ? R.fine().res : R.x; };
+    halo_vec(h, h->nc, src);
+    apply_dot_fine(h, src, [&](Rank& R) { return R.fine().u[1]; }, kRedPlain, true);
+    Rank& R0 = *h->ranks[0];
+    CK(cudaMemcpyAsync(R0.scal_host, R0.scal, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
-    *out = *h->scal_host;
+    *out = *R0.scal_host;
   });
 }
 
 int tmg_gpu_element_energies(tmg_gpu_handle* h, const double* u, double* out) {
   return guarded(h, [&] {
+    need_single(h, "tmg_gpu_element_energies");
     if (!h->have_problem) fail(TMG_ERR_DIMENSION, "problem not set");
-    Level& F = h->fine();
+    Rank& R = *h->ranks[0];
+    Level& F = R.fine();
     const Grid& g = F.g;
     const long ne = static_cast<long>(g.nx) * g.ny;
-    const double2* src = h->x;
+    const double2* src = R.x;
     if (u) {
-      upload_nodes(h, F.res, u, g);
+      upload_nodes(h->stream, F.res, u, g);
       src = F.res;
     } else if (!h->have_solution) {
       fail(TMG_ERR_DIMENSION, "no resident solution");
     }
-    double* d = grow(h->dense, h->dense_cap, ne);
+    double* d = grow(R.dense, R.dense_cap, ne);
     k_element_energy<<<dim3((g.ny + 127) / 128, g.nx), 128, 0, h->stream>>>(g, src, d);
     CKL();
     h->count();
@@ -966,20 +1449,22 @@ int tmg_gpu_element_energies(tmg_gpu_handle* h, const double* u, double* out) {
 int tmg_gpu_sensitivities(tmg_gpu_handle* h, const double* u, int nphases, const double* alpha,
                           const double* phase_moduli, double penalty, double* out) {
   return guarded(h, [&] {
+    need_single(h, "tmg_gpu_sensitivities");
     if (!h->have_problem) fail(TMG_ERR_DIMENSION, "problem not set");
-    Level& F = h->fine();
+    Rank& R = *h->ranks[0];
+    Level& F = R.fine();
     const Grid& g = F.g;
     const long ne = static_cast<long>(g.nx) * g.ny;
-    const double2* src = h->x;
+    const double2* src = R.x;
     if (u) {
-      upload_nodes(h, F.res, u, g);
+      upload_nodes(h->stream, F.res, u, g);
       src = F.res;
     } else if (!h->have_solution) {
       fail(TMG_ERR_DIMENSION, "no resident solution");
     }
-    double* en = grow(h->dense, h->dense_cap, ne * (nphases + 1));
-    double* da = grow(h->aux, h->aux_cap, ne * nphases);
-    double* dp = grow(h->aux2, h->aux2_cap, nphases);
+    double* en = grow(R.dense, R.dense_cap, ne * (nphases + 1));
+    double* da = grow(R.aux, R.aux_cap, ne * nphases);
+    double* dp = grow(R.aux2, R.aux2_cap, nphases);
     CK(cudaMemcpyAsync(da, alpha, sizeof(double) * ne * nphases, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(dp, phase_moduli, sizeof(double) * nphases, cudaMemcpyHostToDevice, h->stream));
     k_element_energy<<<dim3((g.ny + 127) / 128, g.nx), 128, 0, h->stream>>>(g, src, en);
@@ -993,10 +1478,12 @@ int tmg_gpu_sensitivities(tmg_gpu_handle* h, const double* u, int nphases, const
   });
 }
 
-int tmg_gpu_filter(tmg_gpu_handle* h, int nphases, const double* alpha, int phase, double radius,
-                   const double* raw, double* out) {
+int tmg_gpu_filter(tmg_gpu_handle* h, int nphases, const double* alpha, int phase, double radius, const double* raw,
+                   double* out) {
   return guarded(h, [&] {
-    const Grid& g = h->fine().g;
+    need_single(h, "tmg_gpu_filter");
+    Rank& R = *h->ranks[0];
+    const Grid& g = R.fine().g;
     const long ne = static_cast<long>(g.nx) * g.ny;
     if (phase < 0 || phase >= nphases) fail(TMG_ERR_DIMENSION, "filter: phase out of range");
     if (radius <= 1.0) {  // only the self weight survives (mto.cpp:95)
@@ -1004,12 +1491,12 @@ int tmg_gpu_filter(tmg_gpu_handle* h, int nphases, const double* alpha, int phas
       return;
     }
     const int reach = static_cast<int>(std::ceil(radius)) - 1;
-    double* da = grow(h->aux, h->aux_cap, ne * nphases);
-    double* d = grow(h->dense, h->dense_cap, 2 * ne);
+    double* da = grow(R.aux, R.aux_cap, ne * nphases);
+    double* d = grow(R.dense, R.dense_cap, 2 * ne);
     CK(cudaMemcpyAsync(da, alpha, sizeof(double) * ne * nphases, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(d, raw, sizeof(double) * ne, cudaMemcpyHostToDevice, h->stream));
-    k_filter<<<dim3((g.ny + 127) / 128, g.nx), 128, 0, h->stream>>>(g.nx, g.ny, nphases, phase, radius,
-                                                                     reach, da, d, d + ne);
+    k_filter<<<dim3((g.ny + 127) / 128, g.nx), 128, 0, h->stream>>>(g.nx, g.ny, nphases, phase, radius, reach, da, d,
+                                                                     d + ne);
     CKL();
     h->count();
     CK(cudaMemcpyAsync(out, d + ne, sizeof(double) * ne, cudaMemcpyDeviceToHost, h->stream));
@@ -1019,59 +1506,34 @@ int tmg_gpu_filter(tmg_gpu_handle* h, int nphases, const double* alpha, int phas
 
 int tmg_gpu_apply(tmg_gpu_handle* h, int level, const double* x, double* y) {
   return guarded(h, [&] {
+    need_single(h, "tmg_gpu_apply");
     check_level(h, level);
     if (level < h->nc) need_setup(h);
     if (!h->have_moduli || !h->have_problem) fail(TMG_ERR_DIMENSION, "operator not set");
-    Level& L = h->lev[level];
-    upload_nodes(h, L.u[0], x, L.g);
-    apply_level(h, level, L.u[0], L.res);
-    download_nodes(h, y, L.res, L.g);
+    Rank& R = *h->ranks[0];
+    Level& L = R.lev[level];
+    upload_nodes(h->stream, L.u[0], x, L.g);
+    apply_level(h, R, level, L.u[0], L.res);
+    download_nodes(h->stream, y, L.res, L.g);
+    CK(cudaStreamSynchronize(h->stream));
   });
 }
 
-}  // extern "C"
-
-namespace {
-template <class Op>
-__global__ void k_level_values(Op op, Grid g, long n, const int* __restrict__ off,
-                               const int* __restrict__ cols, double* __restrict__ vals) {
-  const long r = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
-  if (r >= n) return;
-  const long node = r >> 1;
-  const int c = static_cast<int>(r & 1);
-  const int x = static_cast<int>(node / (g.ny + 1)), y = static_cast<int>(node % (g.ny + 1));
-  const long i = g.idx(x, y);
-  for (int k = off[r]; k < off[r + 1]; ++k) {
-    const long cn = cols[k] >> 1;
-    const int d = cols[k] & 1;
-    const int ex = static_cast<int>(cn / (g.ny + 1)) - x, ey = static_cast<int>(cn % (g.ny + 1)) - y;
-    double v = 0.0;
-    if (ex >= -1 && ex <= 1 && ey >= -1 && ey <= 1) {
-      double b[4];
-      op.block(i, ex, ey, b);
-      v = b[2 * c + d];
-    }
-    vals[k] = v;
-  }
-}
-}  // namespace
-
-extern "C" {
-
-int tmg_gpu_level_values(tmg_gpu_handle* h, int level, const int* offsets, const int* cols,
-                         double* vals) {
+int tmg_gpu_level_values(tmg_gpu_handle* h, int level, const int* offsets, const int* cols, double* vals) {
   return guarded(h, [&] {
+    need_single(h, "tmg_gpu_level_values");
     check_level(h, level);
     if (level < h->nc) need_setup(h);
-    const Level& L = h->lev[level];
+    Rank& R = *h->ranks[0];
+    const Level& L = R.lev[level];
     const long n = L.ndof;
     const long nnz = offsets[n];
-    int* doff = reinterpret_cast<int*>(grow(h->aux, h->aux_cap, (n + 1 + nnz + 1) / 2 + 1));
+    int* doff = reinterpret_cast<int*>(grow(R.aux, R.aux_cap, (n + 1 + nnz + 1) / 2 + 1));
     int* dcol = doff + n + 1;
-    double* dv = grow(h->dense, h->dense_cap, nnz);
+    double* dv = grow(R.dense, R.dense_cap, nnz);
     CK(cudaMemcpyAsync(doff, offsets, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(dcol, cols, sizeof(int) * nnz, cudaMemcpyHostToDevice, h->stream));
-    with_op(h, level, [&](auto op) {
+    with_op(R, level, [&](auto op) {
       k_level_values<decltype(op)><<<(n + 127) / 128, 128, 0, h->stream>>>(op, L.g, n, doff, dcol, dv);
     });
     CKL();
@@ -1081,57 +1543,69 @@ int tmg_gpu_level_values(tmg_gpu_handle* h, int level, const int* offsets, const
   });
 }
 
-int tmg_gpu_vcycle(tmg_gpu_handle* h, const double* f, double* u, int gamma, int pre_sweeps,
-                   int post_sweeps) {
+int tmg_gpu_vcycle(tmg_gpu_handle* h, const double* f, double* u, int gamma, int pre_sweeps, int post_sweeps) {
   return guarded(h, [&] {
     need_setup(h);
-    Level& F = h->fine();
-    upload_nodes(h, h->r, f, F.g);
-    for (Level& L : h->lev) L.cur = 0;
-    upload_nodes(h, F.u[0], u, F.g);
-    enqueue_cycle(h, h->nc, false, gamma, pre_sweeps, post_sweeps);
-    download_nodes(h, u, F.u[F.cur], F.g);
+    const int nc = h->nc;
+    for (Rank* R : h->ranks) {
+      for (Level& L : R->lev) L.cur = 0;
+      upload_nodes(h->stream, R->r, f, R->fine().g);
+      upload_nodes(h->stream, R->fine().u[0], u, R->fine().g);
+    }
+    halo_vec(h, nc, [&](Rank& R) { return R.r; });
+    enqueue_cycle(h, nc, false, gamma, pre_sweeps, post_sweeps);
+    for (Rank* R : h->ranks) download_nodes(h->stream, u, R->fine().u[R->fine().cur], R->fine().g);
+    CK(cudaStreamSynchronize(h->stream));
   });
 }
 
 int tmg_gpu_prolongate(tmg_gpu_handle* h, int level, const double* coarse, double* fine) {
   return guarded(h, [&] {
+    need_single(h, "tmg_gpu_prolongate");
     check_level(h, level);
     if (level < 1) fail(TMG_ERR_DIMENSION, "prolongate: level " + std::to_string(level) + " has no coarser neighbor");
-    Level& F = h->lev[level];
-    Level& C = h->lev[level - 1];
-    upload_nodes(h, C.u[0], coarse, C.g);
-    prolong_level(h, level, C.u[0], F.res, false);
-    download_nodes(h, fine, F.res, F.g);
+    Rank& R = *h->ranks[0];
+    Level& F = R.lev[level];
+    Level& C = R.lev[level - 1];
+    upload_nodes(h->stream, C.u[0], coarse, C.g);
+    prolong_level(h, R, level, C.u[0], F.res, false);
+    download_nodes(h->stream, fine, F.res, F.g);
+    CK(cudaStreamSynchronize(h->stream));
   });
 }
 
 int tmg_gpu_restrict(tmg_gpu_handle* h, int level, const double* fine, double* coarse) {
   return guarded(h, [&] {
+    need_single(h, "tmg_gpu_restrict");
     check_level(h, level);
     if (level < 1) fail(TMG_ERR_DIMENSION, "restrict: level " + std::to_string(level) + " has no coarser neighbor");
-    Level& F = h->lev[level];
-    Level& C = h->lev[level - 1];
-    upload_nodes(h, F.res, fine, F.g);
-    restrict_level(h, level, F.res, C.res);
-    download_nodes(h, coarse, C.res, C.g);
+    Rank& R = *h->ranks[0];
+    Level& F = R.lev[level];
+    Level& C = R.lev[level - 1];
+    upload_nodes(h->stream, F.res, fine, F.g);
+    restrict_level(h, R, level, F.res, C.res);
+    download_nodes(h->stream, coarse, C.res, C.g);
+    CK(cudaStreamSynchronize(h->stream));
   });
 }
 
 int tmg_gpu_smooth(tmg_gpu_handle* h, int level, const double* f, double* u, int sweeps) {
   return guarded(h, [&] {
+    need_single(h, "tmg_gpu_smooth");
     check_level(h, level);
     if (level < h->nc) need_setup(h);
     if (!h->have_moduli || !h->have_problem) fail(TMG_ERR_DIMENSION, "operator not set");
-    Level& L = h->lev[level];
-    upload_nodes(h, L.f, f, L.g);
-    upload_nodes(h, L.u[0], u, L.g);
+    Rank& R = *h->ranks[0];
+    Level& L = R.lev[level];
+    upload_nodes(h->stream, L.f, f, L.g);
+    upload_nodes(h->stream, L.u[0], u, L.g);
     L.cur = 0;
     for (int s = 0; s < sweeps; ++s) {
-      sweep_level(h, level, false, L.u[L.cur], L.u[L.cur ^ 1], L.f);
+      sweep_level(h, R, level, false, L.u[L.cur], L.u[L.cur ^ 1], L.f);
       L.cur ^= 1;
     }
-    download_nodes(h, u, L.u[L.cur], L.g);
+    download_nodes(h->stream, u, L.u[L.cur], L.g);
+    CK(cudaStreamSynchronize(h->stream));
   });
 }
 
@@ -1142,11 +1616,12 @@ long tmg_gpu_launch_count(tmg_gpu_handle* h) { return h ? h->launches : 0; }
 int tmg_gpu_time_kernel(tmg_gpu_handle* h, int which, int reps, double* avg_ms, double* bytes) {
   return guarded(h, [&] {
     if (!h->have_moduli || !h->have_problem) fail(TMG_ERR_DIMENSION, "operator not set");
-    Level& F = h->fine();
-    const double nodes = static_cast<double>(F.g.nx + 1) * (F.g.ny + 1);
+    Rank& R = *h->ranks[0];
+    Level& F = R.fine();
+    const double nodes = static_cast<double>(F.g.ncol) * (F.g.ny + 1);
     auto launch = [&] {
-      if (which == 0) apply_level(h, h->nc, h->pbuf[0], h->ap);
-      else sweep_level(h, h->nc, false, F.u[0], F.u[1], h->r);
+      if (which == 0) apply_level(h, R, h->nc, R.pbuf[0], R.ap);
+      else sweep_level(h, R, h->nc, false, F.u[0], F.u[1], R.r);
     };
     for (int w = 0; w < 3; ++w) launch();
     CK(cudaEventRecord(h->ev[2], h->stream));

@@ -59,6 +59,8 @@ struct HostMirror {
 
 enum RedOp { kRedNone = 0, kRedZr = 1, kRedPap = 2, kRedRr = 3, kRedB = 4, kRedPlain = 5 };
 
+__device__ __forceinline__ void apply_scalar(RedOp op, double acc, PcgState* st, HostMirror* hm, double* out);
+
 // Final stage: the last block to finish sums all partials in index order.
 // Deterministic for a fixed grid: the order never depends on which block
 // arrives last.
@@ -84,6 +86,13 @@ __device__ __forceinline__ void finish_reduction(double part, double* partials,
   acc = block_sum<NT>(acc);
   if (t != 0) return;
   *ticket = 0u;
+  apply_scalar(op, acc, st, hm, out);
+}
+
+// Scalar tail of a reduction: the global sum `acc` updates the PCG state
+// (single rank: called by the last block; several ranks: by k_scalar after
+// the all-reduce of the per-rank partials).
+__device__ __forceinline__ void apply_scalar(RedOp op, double acc, PcgState* st, HostMirror* hm, double* out) {
   if (out) *out = acc;
   if (!st) return;
   switch (op) {
@@ -124,6 +133,17 @@ __device__ __forceinline__ void finish_reduction(double part, double* partials,
     default:
       break;
   }
+}
+
+// Multi-rank reductions: every rank's partial sums to one global value in
+// rank order (deterministic), then the scalar tail runs on each rank's state.
+__global__ void k_scalar(RedOp op, const double* gsum, PcgState* st, HostMirror* hm, double* out) {
+  apply_scalar(op, *gsum, st, hm, out);
+}
+__global__ void k_sum_ranks(const double* const* parts, int n, double* const* outs) {
+  double s = 0.0;
+  for (int r = 0; r < n; ++r) s += *parts[r];
+  for (int r = 0; r < n; ++r) *outs[r] = s;
 }
 
 // --------------------------------------------------------- node kernels --
@@ -487,7 +507,8 @@ __global__ void __launch_bounds__(kRedThreads) k_update_xr(double2* __restrict__
                                                            const double2* __restrict__ p,
                                                            const double2* __restrict__ ap, long n2,
                                                            double* partials, unsigned* ticket,
-                                                           PcgState* st, HostMirror* hm) {
+                                                           RedOp rop, PcgState* st, HostMirror* hm,
+                                                           double* out) {
   const double alpha = st->alpha;
   double s = 0.0;
   for (long k = blockIdx.x * static_cast<long>(kRedThreads) + threadIdx.x; k < n2;
@@ -503,7 +524,7 @@ __global__ void __launch_bounds__(kRedThreads) k_update_xr(double2* __restrict__
     s = fma(rr.x, rr.x, s);
     s = fma(rr.y, rr.y, s);
   }
-  finish_reduction<kRedThreads>(s, partials, ticket, gridDim.x, kRedRr, st, hm, nullptr);
+  finish_reduction<kRedThreads>(s, partials, ticket, gridDim.x, rop, st, hm, out);
 }
 
 // r = b - t (t = A x0) ; plain copy when t == nullptr
@@ -602,6 +623,30 @@ __global__ void k_filter(int nx, int ny, int np, int phase, double radius, int r
     }
   const long e = static_cast<long>(ex) * ny + ey;
   out[e] = acc / (alpha[e * np + phase] * ws);
+}
+
+// values of a level operator at the entries of a CSR pattern (parity tests)
+template <class Op>
+__global__ void k_level_values(Op op, Grid g, long n, const int* __restrict__ off,
+                               const int* __restrict__ cols, double* __restrict__ vals) {
+  const long r = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+  if (r >= n) return;
+  const long node = r >> 1;
+  const int c = static_cast<int>(r & 1);
+  const int x = static_cast<int>(node / (g.ny + 1)), y = static_cast<int>(node % (g.ny + 1));
+  const long i = g.idx(x, y);
+  for (int k = off[r]; k < off[r + 1]; ++k) {
+    const long cn = cols[k] >> 1;
+    const int d = cols[k] & 1;
+    const int ex = static_cast<int>(cn / (g.ny + 1)) - x, ey = static_cast<int>(cn % (g.ny + 1)) - y;
+    double v = 0.0;
+    if (ex >= -1 && ex <= 1 && ey >= -1 && ey <= 1) {
+      double b[4];
+      op.block(i, ex, ey, b);
+      v = b[2 * c + d];
+    }
+    vals[k] = v;
+  }
 }
 
 }  // namespace tmg

@@ -235,14 +235,27 @@ class MultigridOperators:
     """
 
     def __init__(self, grid: GridLevel, num_coarsenings: int, poisson_ratio: float,
-                 bc: BoundaryConditions, device: int = 0):
+                 bc: BoundaryConditions, device: int = 0, slabs: int = 1, replicated_level: int = -1,
+                 nccl: tuple | None = None):
+        """slabs > 1: the x-slab decomposition driven from this process on one
+        device; nccl=(nranks, rank, unique_id_bytes): one rank of a
+        multi-process (torchrun) solve."""
         self.lib = _lib.load()
         self.grid = grid
         self.num_coarsenings = num_coarsenings
         self.omega = 0.6
         h = C.c_void_p()
-        st = self.lib.tmg_gpu_create(grid.nx, grid.ny, num_coarsenings, grid.dofs_per_node, device,
-                                     C.byref(h))
+        if nccl is not None:
+            nranks, rank, uid = nccl
+            buf = C.create_string_buffer(bytes(uid), 128)
+            st = self.lib.tmg_gpu_create_nccl(grid.nx, grid.ny, num_coarsenings, grid.dofs_per_node, device,
+                                              nranks, rank, buf, replicated_level, C.byref(h))
+        elif slabs > 1:
+            st = self.lib.tmg_gpu_create_local_slabs(grid.nx, grid.ny, num_coarsenings, grid.dofs_per_node,
+                                                     device, slabs, replicated_level, C.byref(h))
+        else:
+            st = self.lib.tmg_gpu_create(grid.nx, grid.ny, num_coarsenings, grid.dofs_per_node, device,
+                                         C.byref(h))
         self.h = h
         if st != 0:
             msg, row = self._err()
@@ -349,6 +362,24 @@ class MultigridOperators:
         p = C.c_double()
         self.lib.tmg_gpu_last_timings(self.h, C.byref(s), C.byref(p))
         return s.value, p.value
+
+
+def slab_partition(nx: int, num_coarsenings: int, nranks: int, replicated_level: int = -1):
+    """(first fine node column of every rank + [nx+1], replicated level)."""
+    x0s = np.zeros(nranks + 1, np.int32)
+    rep = C.c_int()
+    st = _lib.load().tmg_partition(nx, num_coarsenings, nranks, replicated_level, iptr(x0s), C.byref(rep))
+    if st != 0:
+        _raise(st, "tmg_partition failed")
+    return x0s.tolist(), rep.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = _lib.load().tmg_nccl_unique_id(buf)
+    if st != 0:
+        _raise(st, "ncclGetUniqueId failed")
+    return buf.raw
 
 
 def build_multigrid_operators(grid: GridLevel, moduli: np.ndarray, poisson_ratio: float,

@@ -1,0 +1,77 @@
+"""The x-slab decomposition run end to end on one B200:
+several ranks in one process exchange halos by device copies and sum the PCG
+scalars in rank order (LocalComm); the NCCL path differs only in the
+transport. The decomposed solve must reproduce the single-rank solve and the
+CPU checker to the north-star bars."""
+import numpy as np
+import pytest
+
+import paper_2301_07457_b200 as P
+from helpers import MAT, moduli, rel
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+
+def build(nx, ny, nc, slabs, rep=-1, recipe="iid", seed=0):
+    _, E = moduli(nx, ny, recipe, seed)
+    g = P.GridLevel(nx, ny)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    ops = P.MultigridOperators(g, nc, 0.3, bc, slabs=slabs, replicated_level=rep)
+    ops.set_moduli(E, 0.6)
+    return ops, E, bc, P.assemble_rhs(g, bc)
+
+
+CASES = [
+    # nx, ny, coarsenings, slabs, replicated level (-1 = auto)
+    (64, 32, 3, 2, 1),
+    (64, 64, 3, 2, -1),
+    (128, 64, 4, 3, 1),
+    (128, 128, 5, 4, 2),
+    (256, 64, 5, 2, 3),
+]
+
+
+@pytest.mark.parametrize("nx,ny,nc,slabs,rep", CASES)
+def test_slab_solve_matches_single_rank_and_reference(nx, ny, nc, slabs, rep):
+    one, E, bc, b = build(nx, ny, nc, 1)
+    many, _, _, _ = build(nx, ny, nc, slabs, rep)
+    cfg = P.SolverConfig(tol=1e-8, max_iter=500)
+    r1 = P.pcgmg_solve(one, b, cfg)
+    rn = P.pcgmg_solve(many, b, cfg)
+    ref = po.System("orc", nx, ny, E, 0.3, bc.fixed_dofs, bc.point_loads).build_mg(nc).solve(b, tol=1e-8)
+    assert rn.converged
+    assert abs(rn.iterations - r1.iterations) <= 1
+    assert abs(rn.iterations - ref["iterations"]) <= 2
+    assert rel(rn.solution, r1.solution) <= 1e-10
+    assert rel(rn.solution, ref["solution"]) <= 1e-8
+    c1, cn = P.compliance(one), P.compliance(many)
+    assert abs(cn - c1) <= 1e-12 * abs(c1)
+
+
+@pytest.mark.parametrize("gamma,sweeps", [(1, 2), (2, 1), (1, 1), (2, 2)])
+def test_slab_cycle_matches_single_rank(gamma, sweeps):
+    nx, ny, nc = 128, 64, 4
+    one, _, _, _ = build(nx, ny, nc, 1)
+    many, _, _, _ = build(nx, ny, nc, 3, 1)
+    rng = np.random.default_rng(21)
+    f = rng.standard_normal(2 * (nx + 1) * (ny + 1))
+    for u0 in (np.zeros_like(f), rng.standard_normal(f.size)):
+        a = P.mg_cycle(one, u0, f, gamma, sweeps, sweeps)
+        b = P.mg_cycle(many, u0, f, gamma, sweeps, sweeps)
+        assert rel(b, a) <= 1e-12
+
+
+def test_slab_warm_start_and_determinism():
+    nx, ny, nc = 128, 64, 4
+    many, E, bc, b = build(nx, ny, nc, 2, 2)
+    cfg = P.SolverConfig(tol=1e-8, max_iter=500)
+    first = P.pcgmg_solve(many, b, cfg)
+    again = P.pcgmg_solve(many, b, cfg)
+    assert first.residual_history == again.residual_history
+    assert np.array_equal(first.solution, again.solution)
+    warm = P.pcgmg_solve(many, b, cfg, x0=first.solution * 0.98)
+    ref = po.System("orc", nx, ny, E, 0.3, bc.fixed_dofs, bc.point_loads).build_mg(nc).solve(
+        b, tol=1e-8, x0=first.solution * 0.98)
+    assert abs(warm.iterations - ref["iterations"]) <= 2
+    assert rel(warm.solution, ref["solution"]) <= 1e-8
