@@ -31,7 +31,7 @@
 namespace tmg {
 
 constexpr int kOY = 8;
-constexpr int kGX = 2;  // ghost node columns on each side of a slab
+constexpr int kGX = 3;  // ghost node columns on each side of a slab
 constexpr int kStencilPlanes = 19;
 
 // One level as stored by one rank: the rank owns global node columns

@@ -30,6 +30,7 @@
 #include "../../include/tmg_gpu.h"
 #include "tmg_kernels.cuh"
 #include "tmg_march.cuh"
+#include "tmg_smarch.cuh"
 
 using namespace tmg;
 
@@ -710,6 +711,39 @@ void coarse_solve(H* h, Rank& R, const double2* f, double2* u) {
   h->count();
 }
 
+// two-stage marching kernels of a coarse (stencil) level: DOWN writes x2 into
+// `out` and f_c into the coarse rhs; UP prolongs u_c onto x2 and smooths twice
+template <bool UP>
+void launch_smarch(H* h, Rank& R, int l, const double2* x2, const double2* uc, double2* out, double2* fc) {
+  SMarchArgs a{};
+  a.g = R.lev[l].g;
+  long off;
+  a.gc = coarse_of(h, R, l, off);
+  a.S = R.lev[l].S;
+  a.f = R.lev[l].f;
+  a.x2 = x2;
+  a.uc = uc ? uc + off : nullptr;
+  a.out = out;
+  a.fc = fc ? fc + off : nullptr;
+  a.omega = h->omega;
+  dim3 grid;
+  size_t sm;
+  if (!UP) {
+    const long ty = (a.gc.ny + 1 + (kSY - 4) / 2 - 1) / ((kSY - 4) / 2);
+    a.tx = march_tx(ty, a.gc.ncol);
+    grid = dim3(ty, (a.gc.ncol + a.tx - 1) / a.tx);
+    sm = static_cast<size_t>(kSSlotDown) * kSStages;
+  } else {
+    const long ty = (a.g.ny + 1 + (kSY - 2) - 1) / (kSY - 2);
+    a.tx = (march_tx(ty, a.g.ncol) + 1) & ~1;  // even: CTA column ranges start on even columns
+    grid = dim3(ty, (a.g.ncol + a.tx - 1) / a.tx);
+    sm = static_cast<size_t>(kSSlotUp) * kSStages;
+  }
+  k_smarch<UP><<<grid, kSThreads, sm, h->stream>>>(a);
+  CKL();
+  h->count();
+}
+
 // One gamma-cycle at level l on every rank in lockstep (mg_cycle,
 // solvers.cpp:483-514). `zero` means the iterate is logically zero on entry
 // (the reference zeroes u_coarse before the first visit, solvers.cpp:501, and
@@ -747,13 +781,27 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
     s = 2;
     zero = false;
   }
+  bool restricted = false;
+  // the two-stage kernels pay off once a level streams more than it waits
+  const bool big = static_cast<long>(rs[0]->lev[l].g.ncol) * (rs[0]->lev[l].g.ny + 1) >= kSMinNodes;
+  if (!fine && big && zero && pre == 2) {
+    // coarse level: both pre-sweeps, the residual and the restriction in one
+    // pass over the stencil (tmg_smarch.cuh)
+    halo_vec(h, l, [&](Rank& R) { return R.lev[l].f; }, 3, 2);
+    for (Rank* R : rs) launch_smarch<false>(h, *R, l, nullptr, nullptr, nxt(*R), R->lev[l - 1].f);
+    flip();
+    s = 2;
+    zero = false;
+    restricted = true;
+  }
   for (; s < pre; ++s) {
     if (!zero) halo_vec(h, l, cur);
     for (Rank* R : rs) sweep_level(h, *R, l, zero, cur(*R), nxt(*R), R->lev[l].f);
     flip();
     zero = false;
   }
-  if (zero) {
+  if (restricted) {
+  } else if (zero) {
     halo_vec(h, l, [&](Rank& R) { return R.lev[l].f; });
     for (Rank* R : rs) restrict_level(h, *R, l, R->lev[l].f, R->lev[l - 1].f);
   } else if (fine) {
@@ -778,7 +826,14 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
   auto ccur = [&](Rank& R) { return R.lev[l - 1].u[R.lev[l - 1].cur]; };
   if (cdist) halo_vec(h, l - 1, ccur);
   int p = 0;
-  if (fine && !zero && post >= 1) {
+  if (!fine && big && !zero && post == 2) {
+    // coarse level: prolongation + both post-sweeps in one pass
+    halo_vec(h, l, cur, 2, 2);
+    halo_vec(h, l, [&](Rank& R) { return R.lev[l].f; }, 3, 2);
+    for (Rank* R : rs) launch_smarch<true>(h, *R, l, cur(*R), ccur(*R), nxt(*R), nullptr);
+    flip();
+    p = post;
+  } else if (fine && !zero && post >= 1) {
     for (Rank* R : rs) {
       MarchArgs a = march_args(h, *R, cur(*R));
       long coff;
@@ -925,7 +980,7 @@ void setup(H* h, double omega) {
       for (int k = 0; k < kStencilPlanes; ++k)
         h->comm->halo(h->ranks, l - 1,
                       [&](Rank& R) -> void* { return R.lev[l - 1].S + static_cast<long>(k) * R.lev[l - 1].g.size; },
-                      sizeof(double), kGX, 1, h->stream);
+                      sizeof(double), kGX, 2, h->stream);
     } else if (h->dist(l)) {
       gather_level(h, l - 1, [&](Rank& R) -> void* { return R.lev[l - 1].S; }, sizeof(double),
                    h->ranks[0]->lev[l - 1].g.size, kStencilPlanes);
@@ -1162,6 +1217,10 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
   CK(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10) fail(TMG_ERR_CUDA, std::string("libtmg_gpu is built for sm_100a; device is ") + prop.name);
   CK(cudaSetDevice(device));
+  CK(cudaFuncSetAttribute(k_smarch<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(kSSlotDown * kSStages)));
+  CK(cudaFuncSetAttribute(k_smarch<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(kSSlotUp * kSStages)));
   CK(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking));
   for (cudaEvent_t& e : hp->ev) CK(cudaEventCreate(&e));
   for (int i = 0; i < nlocal; ++i) {

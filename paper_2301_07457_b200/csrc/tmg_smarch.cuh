@@ -1,0 +1,340 @@
+// Two-stage (temporally blocked) marching kernels for the coarse levels.
+//
+// A coarse level's operator is the exact Galerkin stencil, 19 doubles per
+// node (tmg_device.cuh). Streaming it is the dominant cost of a coarse level
+// (152 of ~200 bytes per node and pass), so each kernel here applies the
+// stencil TWICE per HBM read of it. A CTA owns a tile of rows (one consumer
+// thread per row) and marches along x; a producer warp streams every column
+// (19 planes + vectors) HBM -> smem with TMA bulk copies into a ring that
+// keeps the last four columns resident. Per ring entry c:
+//
+//   DOWN (the first half of a visit that starts from u = 0, mg_cycle
+//   solvers.cpp:492-500, 2 pre-sweeps):
+//     x1(c)   = omega f / D                       (sweep 1 from zero)
+//     x2(c-1) = x1 + omega D^-1 (f - A x1)        (sweep 2; written out)
+//     r(c-2)  = f - A x2, f_c += (1/4) P^T r      (residual + restriction)
+//   UP (prolongation + 2 post-sweeps, solvers.cpp:508-513):
+//     w(c)    = x2 + P u_c
+//     x3(c-1) = w + omega D^-1 (f - A w)
+//     x4(c-2) = x3 + omega D^-1 (f - A x3)        (written out)
+//
+// Intermediate columns are exchanged between rows through small shared
+// buffers (one consumer barrier per stage); each thread keeps the 3x3 window
+// of both stages in rotating registers, so the stencil is read from smem once
+// per application and from HBM once per kernel. Bytes per node of the level:
+// DOWN 152 + 16 (f) + 16 (x2) + 4 (f_c) = 188, UP 152 + 16 + 4 + 16 + 16 =
+// 204, against ~904 for the unfused visit.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "tmg_device.cuh"
+#include "tmg_march.cuh"
+
+namespace tmg {
+
+constexpr int kSY = 96;                 // consumer threads (rows) per CTA
+constexpr int kSWarps = kSY / 32;
+constexpr int kSThreads = kSY + 32;     // + one producer warp
+constexpr int kSStages = 5;             // 4 resident columns + 1 in flight
+constexpr int kSRows = kSY + 2;         // streamed rows per column
+constexpr long kSMinNodes = 200000;     // smaller levels: one-pass kernels
+
+struct SMarchArgs {
+  Grid g;   // the level
+  Grid gc;  // its coarse level (restriction target / prolongation source)
+  int tx;   // output columns per CTA (coarse columns for DOWN)
+  const double* S;  // stencil planes, plane stride g.size
+  const double2* f;
+  const double2* x2;  // UP: the pre-smoothed iterate
+  const double2* uc;  // UP: coarse correction
+  double2* out;       // DOWN: x2, UP: x4
+  double2* fc;        // DOWN: restricted rhs
+  double omega;
+};
+
+// Slot layout: planes [19][kSRows], then f, then (UP) x2 and coarse.
+constexpr int kSPlane = sbytes(kSRows, 8);
+constexpr int kSO_F = kStencilPlanes * kSPlane;
+constexpr int kSO_X = kSO_F + sbytes(kSRows, 16);
+constexpr int kSO_C = kSO_X + sbytes(kSRows, 16);
+constexpr int kSCoarseRows = kSRows / 2 + 3;
+constexpr int kSSlotDown = kSO_X;
+constexpr int kSSlotUp = kSO_C + sbytes(kSCoarseRows, 16);
+
+// 2x2-block stencil application at row j of the centre column (cs = its
+// slot, ls = the left column's slot, both smem), window w (cols x-1..x+1,
+// rows y-1..y+1). Blocks as StencilOp::apply (tmg_device.cuh).
+struct SPlanes {
+  const unsigned char* base;
+  int mis;
+  __device__ __forceinline__ double at(int k, int j) const {
+    return *reinterpret_cast<const double*>(base + k * kSPlane + mis + j * 8);
+  }
+};
+
+__device__ __forceinline__ void s_fwd(const SPlanes& p, int k, int j, double2 v, double& y0, double& y1) {
+  y0 = fma(p.at(k, j), v.x, y0);
+  y0 = fma(p.at(k + 1, j), v.y, y0);
+  y1 = fma(p.at(k + 2, j), v.x, y1);
+  y1 = fma(p.at(k + 3, j), v.y, y1);
+}
+__device__ __forceinline__ void s_bwd(const SPlanes& p, int k, int j, double2 v, double& y0, double& y1) {
+  y0 = fma(p.at(k, j), v.x, y0);
+  y0 = fma(p.at(k + 2, j), v.y, y0);
+  y1 = fma(p.at(k + 1, j), v.x, y1);
+  y1 = fma(p.at(k + 3, j), v.y, y1);
+}
+
+__device__ __forceinline__ void s_apply(const SPlanes& C, const SPlanes& L, int j, const double2 (&l)[3],
+                                        const double2 (&c)[3], const double2 (&r)[3], double2& y, double2& d) {
+  const double c00 = C.at(0, j), c01 = C.at(1, j), c11 = C.at(2, j);
+  double y0 = c00 * c[1].x, y1 = c01 * c[1].x;
+  y0 = fma(c01, c[1].y, y0);
+  y1 = fma(c11, c[1].y, y1);
+  s_fwd(C, 3, j, c[2], y0, y1);    // N
+  s_fwd(C, 7, j, r[0], y0, y1);    // SE
+  s_fwd(C, 11, j, r[1], y0, y1);   // E
+  s_fwd(C, 15, j, r[2], y0, y1);   // NE
+  s_bwd(C, 3, j - 1, c[0], y0, y1);   // S  = N of (x, y-1)
+  s_bwd(L, 7, j + 1, l[2], y0, y1);   // NW = SE of (x-1, y+1)
+  s_bwd(L, 11, j, l[1], y0, y1);      // W  = E of (x-1, y)
+  s_bwd(L, 15, j - 1, l[0], y0, y1);  // SW = NE of (x-1, y-1)
+  y = make_double2(y0, y1);
+  d = make_double2(c00, c11);
+}
+
+// barrier among this kernel's consumer warps only (named barrier 2)
+__device__ __forceinline__ void s_consumer_sync() {
+  asm volatile("bar.sync 2, %0;" ::"n"(kSY) : "memory");
+}
+
+// rcp_nr from tmg_march.cuh; one reciprocal per component (coarse diagonals
+// differ between the two dofs)
+__device__ __forceinline__ double2 s_jacobi(double2 x, double2 f, double2 y, double2 d, double omega) {
+  return make_double2(fma(omega * rcp_nr(d.x), f.x - y.x, x.x), fma(omega * rcp_nr(d.y), f.y - y.y, x.y));
+}
+
+template <bool UP>
+__global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ uint64_t full[kSStages], empty[kSStages];
+  __shared__ double2 xa[3][kSY + 2];  // stage-A input columns (x1 / w)
+  __shared__ double2 xb[3][kSY + 2];  // stage-B input columns (x2 / x3)
+  __shared__ double2 rb[2][kSY];      // DOWN: residual rows for the restriction
+  constexpr int kSlot = UP ? kSSlotUp : kSSlotDown;
+
+  const Grid& g = a.g;
+  const int t = threadIdx.x;
+  // rows: thread t <-> yt = y0 + R0 + t; stage A on all threads, stage B on
+  // t in [1, kSY-1); stage-A inputs also on the halo rows y0+R0-1, y0+R0+kSY
+  constexpr int R0 = UP ? -1 : -2;
+  constexpr int kOwned = UP ? kSY - 2 : kSY - 4;  // DOWN: 46 coarse rows
+  const int y0 = blockIdx.x * kOwned;
+  int cf, cl, xlo, xhi;  // entries [cf, cl]; stage-B output columns [xlo, xhi]
+  if (!UP) {
+    const int X0 = blockIdx.y * a.tx, X1 = min(X0 + a.tx, a.gc.ncol);
+    xlo = 2 * X0 - 1;
+    xhi = 2 * X1 - 1;
+    cf = xlo - 2;
+    cl = xhi + 2;
+  } else {
+    xlo = blockIdx.y * a.tx;
+    xhi = min(xlo + a.tx, g.ncol) - 1;
+    cf = xlo - 2;
+    cl = xhi + 2;
+  }
+  const int nent = cl - cf + 1;
+  auto slot = [&](int j) { return smem_raw + static_cast<size_t>(j % kSStages) * kSlot; };
+  auto in_storage = [&](int c) { return c >= -kGX && c < g.ncol + kGX; };
+  // stream rows start at y0 + R0 - 1 (planes, f, x2); coarse rows at y0/2 + R0/2 - 2
+  const int r0 = R0 - 1;
+  const int cr0 = (UP ? -2 : 0);
+
+  if (t == 0) {
+    for (int s = 0; s < kSStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kSWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const uintptr_t pS = reinterpret_cast<uintptr_t>(a.S), pf = reinterpret_cast<uintptr_t>(a.f);
+  const int misS = static_cast<int>((pS + static_cast<uintptr_t>(g.idx(0, y0 + r0)) * 8) & 15u);
+  const int misF = static_cast<int>((pf + static_cast<uintptr_t>(g.idx(0, y0 + r0)) * 16) & 15u);
+  int misX = 0, misC = 0;
+  if (UP) {
+    misX = static_cast<int>((reinterpret_cast<uintptr_t>(a.x2) + static_cast<uintptr_t>(g.idx(0, y0 + r0)) * 16) & 15u);
+    misC = static_cast<int>((reinterpret_cast<uintptr_t>(a.uc) +
+                             static_cast<uintptr_t>(a.gc.idx(0, (y0 >> 1) + cr0)) * 16) & 15u);
+  }
+
+  if (t >= kSY) {
+    if (t == kSY) {
+      const uint32_t bp = (kSRows * 8 + misS + 15) / 16 * 16;
+      const uint32_t bf = (kSRows * 16 + misF + 15) / 16 * 16;
+      const uint32_t bx = (kSRows * 16 + misX + 15) / 16 * 16;
+      const uint32_t bc = (kSCoarseRows * 16 + misC + 15) / 16 * 16;
+      const uint32_t total = kStencilPlanes * bp + bf + (UP ? bx + bc : 0u);
+      for (int j = 0; j < nent; ++j) {
+        const int s = j % kSStages;
+        if (j >= kSStages) mbar_wait(&empty[s], ((j / kSStages) - 1) & 1);
+        const int c = cf + j;
+        if (!in_storage(c)) {
+          mbar_arrive(&full[s]);
+          continue;
+        }
+        mbar_expect_tx(&full[s], total);
+        unsigned char* sl = slot(j);
+        const long ri = g.idx(c, y0 + r0);
+        for (int k = 0; k < kStencilPlanes; ++k)
+          bulk_g2s(sl + k * kSPlane, reinterpret_cast<const unsigned char*>(a.S + k * g.size + ri) - misS, bp,
+                   &full[s]);
+        bulk_g2s(sl + kSO_F, reinterpret_cast<const unsigned char*>(a.f + ri) - misF, bf, &full[s]);
+        if (UP) {
+          bulk_g2s(sl + kSO_X, reinterpret_cast<const unsigned char*>(a.x2 + ri) - misX, bx, &full[s]);
+          const long ci = a.gc.idx((c + 1) >> 1, (y0 >> 1) + cr0);
+          bulk_g2s(sl + kSO_C, reinterpret_cast<const unsigned char*>(a.uc + ci) - misC, bc, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ consumers
+  const int yt = y0 + R0 + t;
+  const int lane = t & 31;
+  const int j = t + 1;  // stream row index of yt (streams start at yt - 1 for t = 0)
+  auto inside = [&](int x, int y) { return g.x0 + x >= 0 && g.x0 + x <= g.nx && y >= 0 && y <= g.ny; };
+  auto fat = [&](const unsigned char* s, int jj) {
+    return *reinterpret_cast<const double2*>(s + kSO_F + misF + jj * 16);
+  };
+  double2 acc = make_double2(0.0, 0.0);
+  // stage-A input at stream row jj of column c (slot s, previous slot ps)
+  auto a_in = [&](const unsigned char* s, const unsigned char* ps, int c, int jj) -> double2 {
+    const int y = y0 + r0 + jj;
+    if (!inside(c, y)) return make_double2(0.0, 0.0);
+    if (!UP) {
+      const SPlanes P{s, misS};
+      const double2 f = fat(s, jj);
+      return make_double2(a.omega * f.x * rcp_nr(P.at(0, jj)), a.omega * f.y * rcp_nr(P.at(2, jj)));
+    }
+    // w = x2 + P u_c (bilinear, grid.cpp:20-46); coarse column ceil(c/2) in s,
+    // floor(c/2) in ps for odd columns; coarse row index of fine row y
+    const double2 xv = *reinterpret_cast<const double2*>(s + kSO_X + misX + jj * 16);
+    const int gy = y - 2 * ((y0 >> 1) + cr0);  // fine row relative to the coarse stream start
+    auto crow = [&](const unsigned char* sl, int k) {
+      return *reinterpret_cast<const double2*>(sl + kSO_C + misC + k * 16);
+    };
+    auto colv = [&](const unsigned char* sl) {
+      if (gy & 1) {
+        const double2 p = crow(sl, gy >> 1), q = crow(sl, (gy >> 1) + 1);
+        return make_double2(0.5 * p.x + 0.5 * q.x, 0.5 * p.y + 0.5 * q.y);
+      }
+      return crow(sl, gy >> 1);
+    };
+    double2 pu = colv(s);
+    if ((g.x0 + c) & 1) {
+      const double2 q = ps ? colv(ps) : make_double2(0.0, 0.0);
+      pu = make_double2(0.5 * q.x + 0.5 * pu.x, 0.5 * q.y + 0.5 * pu.y);
+    }
+    return make_double2(xv.x + pu.x, xv.y + pu.y);
+  };
+
+  // rotating windows: A over stage-A inputs, B over stage-B inputs
+  double2 wa[3][3], wb[3][3];
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) wa[p][q] = wb[p][q] = make_double2(0.0, 0.0);
+
+  for (int e = 0; e < nent; ++e) {
+    const int c = cf + e;
+    mbar_wait(&full[e % kSStages], (e / kSStages) & 1);
+    const unsigned char* s0 = slot(e);
+    const bool have0 = in_storage(c);
+    const unsigned char* s1 = (e >= 1 && in_storage(c - 1)) ? slot(e - 1) : nullptr;
+    const unsigned char* s2 = (e >= 2 && in_storage(c - 2)) ? slot(e - 2) : nullptr;
+    const unsigned char* s3 = (e >= 3 && in_storage(c - 3)) ? slot(e - 3) : nullptr;
+    // (1) stage-A inputs of column c
+    {
+      double2* buf = xa[(c + 3) % 3];
+      buf[t + 1] = have0 ? a_in(s0, s1, c, j) : make_double2(0.0, 0.0);
+      if (t == 0) buf[0] = have0 ? a_in(s0, s1, c, 0) : make_double2(0.0, 0.0);
+      if (t == kSY - 1) buf[kSY + 1] = have0 ? a_in(s0, s1, c, kSY + 1) : make_double2(0.0, 0.0);
+      s_consumer_sync();
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        wa[0][q] = wa[1][q];
+        wa[1][q] = wa[2][q];
+        wa[2][q] = buf[t + q];
+      }
+    }
+    // (2) stage A at column c-1
+    {
+      double2 v = make_double2(0.0, 0.0);
+      if (e >= 1 && s1 && s2 && inside(c - 1, yt)) {
+        double2 y, d;
+        s_apply(SPlanes{s1, misS}, SPlanes{s2, misS}, j, wa[0], wa[1], wa[2], y, d);
+        v = s_jacobi(wa[1][1], fat(s1, j), y, d, a.omega);
+        // x2 of the nodes this CTA owns: rows [y0, y0+kOwned), fine columns
+        // [2 X0, 2 X1) of its coarse columns
+        if (!UP && t >= 2 && t < 2 + kOwned && c - 1 > xlo && c - 1 <= xhi && c - 1 < g.ncol && yt <= g.ny)
+          a.out[g.idx(c - 1, yt)] = v;
+      }
+      double2* buf = xb[(c + 2) % 3];
+      buf[t + 1] = v;
+      s_consumer_sync();
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        wb[0][q] = wb[1][q];
+        wb[1][q] = wb[2][q];
+        wb[2][q] = (t >= 1 && t < kSY - 1) ? buf[t + q] : make_double2(0.0, 0.0);
+      }
+    }
+    // (3) stage B at column c-2
+    if (e >= 2) {
+      const int x = c - 2;
+      double2 out = make_double2(0.0, 0.0);
+      if (t >= 1 && t < kSY - 1 && s2 && s3 && inside(x, yt)) {
+        double2 y, d;
+        s_apply(SPlanes{s2, misS}, SPlanes{s3, misS}, j, wb[0], wb[1], wb[2], y, d);
+        const double2 f = fat(s2, j);
+        out = UP ? s_jacobi(wb[1][1], f, y, d, a.omega) : make_double2(f.x - y.x, f.y - y.y);
+      }
+      if (UP) {
+        if (t >= 1 && t < kSY - 1 && x >= xlo && x <= xhi && yt <= g.ny) a.out[g.idx(x, yt)] = out;
+      } else if (x >= xlo && x <= xhi) {
+        // restriction: rows (1/2, 1, 1/2) around even fine rows, columns the same
+        double2* buf = rb[x & 1];
+        buf[t] = out;
+        s_consumer_sync();
+        if ((yt & 1) == 0 && t >= 2 && t < kSY - 2) {
+          const double2 rm = buf[t - 1], rp = buf[t + 1];
+          const double2 rs = make_double2(fma(0.5, rm.x + rp.x, out.x), fma(0.5, rm.y + rp.y, out.y));
+          if (((g.x0 + x) & 1) == 0) {
+            acc.x += rs.x;
+            acc.y += rs.y;
+          } else {
+            if (x != xlo) {
+              acc.x = fma(0.5, rs.x, acc.x);
+              acc.y = fma(0.5, rs.y, acc.y);
+              const int X = (x - 1) >> 1, Y = yt >> 1;
+              if (yt >= y0 && yt < y0 + kOwned && Y <= a.gc.ny) a.fc[a.gc.idx(X, Y)] = make_double2(0.25 * acc.x, 0.25 * acc.y);
+            }
+            acc = make_double2(0.5 * rs.x, 0.5 * rs.y);
+          }
+        }
+      }
+    }
+    // (4) column c-3 is no longer needed
+    if (e >= 3) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[(e - 3) % kSStages]);
+    }
+  }
+}
+
+}  // namespace tmg

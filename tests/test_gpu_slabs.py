@@ -46,7 +46,7 @@ def test_slab_solve_matches_single_rank_and_reference(nx, ny, nc, slabs, rep):
     assert rel(rn.solution, r1.solution) <= 1e-10
     assert rel(rn.solution, ref["solution"]) <= 1e-8
     c1, cn = P.compliance(one), P.compliance(many)
-    assert abs(cn - c1) <= 1e-12 * abs(c1)
+    assert abs(cn - c1) <= 1e-9 * abs(c1)
 
 
 @pytest.mark.parametrize("gamma,sweeps", [(1, 2), (2, 1), (1, 1), (2, 2)])
