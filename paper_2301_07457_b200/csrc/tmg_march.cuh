@@ -266,6 +266,7 @@ struct Col {
   double2 u[3];
   double e1, e2;  // element column c, rows yt-1, yt
   uint32_t m3;    // mask bytes of rows yt-1, yt, yt+1
+  double2 w;      // StSweep01: omega / D of the own row (reused by the 2nd sweep)
 };
 
 // window field u (rows -1..TY), E (rows -1..TY), M (rows -1..TY)
@@ -380,9 +381,9 @@ struct StSweep01 {
     return {reinterpret_cast<const unsigned char*>(a.M), 1, -1, kTY + 2, false};
   }
   __device__ static int off(int k) { return k == 0 ? O_F : (k == 1 ? O_E : O_M); }
-  // x1 at stream row index j (row y0 - 1 + j) of column c
+  // x1 at stream row index j (row y0 - 1 + j) of column c; *w = omega / D
   __device__ static double2 x1_at(const MarchArgs& a, const unsigned char* s, const unsigned char* ps,
-                                  const int* mis, int j) {
+                                  const int* mis, int j, double2* w) {
     // node rows r = y0-1+j: elements (c-1, r-1), (c, r-1), (c, r), (c-1, r)
     // sit at E-stream indices j and j+1 (stream starts at row y0-2)
     const double eA = ps ? sat<double>(ps, O_E, mis[1], j) : 0.0;
@@ -392,18 +393,25 @@ struct StSweep01 {
     const double2 d = fine_diag(eA, eB, eC, eD, m);
     const double2 f = sat<double2>(s, O_F, mis[0], j);
     // ghost nodes have no elements: D = 0 and x1 = 0
-    if (d.x == 0.0) return make_double2(0.0, 0.0);
+    if (d.x == 0.0) {
+      if (w) *w = make_double2(0.0, 0.0);
+      return make_double2(0.0, 0.0);
+    }
     const double s0 = a.omega * rcp_nr(d.x);
     const double s1 = (d.y == d.x) ? s0 : a.omega * rcp_nr(d.y);
+    if (w) *w = make_double2(s0, s1);
     return make_double2(s0 * f.x, s1 * f.y);
   }
+  // Own row x1 per thread, shared with the neighbouring rows through a
+  // double-buffered smem column (one consumer barrier per column); the first
+  // and last thread also evaluate the halo rows of the tile.
   __device__ static void load(const MarchArgs& a, const unsigned char* s, const unsigned char* ps,
                               const int* mis, int t, int c, Col& col) {
     __shared__ double2 xb[2][kTY + 2];
     double2* buf = xb[c & 1];
-    buf[t + 1] = x1_at(a, s, ps, mis, t + 1);
-    if (t == 0) buf[0] = x1_at(a, s, ps, mis, 0);
-    if (t == kTY - 1) buf[kTY + 1] = x1_at(a, s, ps, mis, kTY + 1);
+    buf[t + 1] = x1_at(a, s, ps, mis, t + 1, &col.w);
+    if (t == 0) buf[0] = x1_at(a, s, ps, mis, 0, nullptr);
+    if (t == kTY - 1) buf[kTY + 1] = x1_at(a, s, ps, mis, kTY + 1, nullptr);
     consumer_sync();
     col.u[0] = buf[t];
     col.u[1] = buf[t + 1];
@@ -419,7 +427,8 @@ struct StSweep01 {
     double2 y, d;
     window_apply(L, C, R, y, d);
     const double2 f = sat<double2>(cs, O_F, mis[0], t + 1);
-    a.out0[a.g.idx(x, yt)] = jacobi_update(C.u[1], f, y, d, a.omega);
+    const double2 x1 = C.u[1];
+    a.out0[a.g.idx(x, yt)] = make_double2(fma(C.w.x, f.x - y.x, x1.x), fma(C.w.y, f.y - y.y, x1.y));
   }
 };
 
@@ -429,7 +438,9 @@ struct StSweep01 {
 // [X0, X0 + tx) and marches fine columns 2 X0 - 1 .. 2 (X0 + tx) - 1.
 struct StResidRestrict : WithF<-1> {
   static constexpr int kOwned = kTY - 2, kLead = 0;
-  // acc: running sum of the coarse column being accumulated
+  // acc: this row's residual summed over the fine columns of the coarse
+  // column being accumulated, with weights (1/2, 1, 1/2) in x; the rows are
+  // combined ((1/2, 1, 1/2) in y) once per coarse column through smem
   __device__ static void run(const MarchArgs& a, const Col& L, const Col& C, const Col& R,
                              const unsigned char* cs, const int* mis, int x, int yt, int t, bool live, double&,
                              double2& acc) {
@@ -441,28 +452,29 @@ struct StResidRestrict : WithF<-1> {
       const double2 f = fc(cs, mis, t);
       r = make_double2(f.x - y.x, f.y - y.y);
     }
-    double2* buf = rbuf[x & 1];
-    buf[t] = r;
-    consumer_sync();
-    // even fine rows (odd t) carry the coarse rows: weights (1/2, 1, 1/2) in y
-    if ((t & 1) && t < kTY - 1) {
-      const double2 rm = buf[t - 1], rp = buf[t + 1];
-      const double2 rs = make_double2(fma(0.5, rm.x + rp.x, r.x), fma(0.5, rm.y + rp.y, r.y));
-      if ((x & 1) == 0) {  // fine column 2X: weight 1
-        acc.x += rs.x;
-        acc.y += rs.y;
-      } else {
-        // fine column 2X+1 closes coarse column X = (x-1)/2 and opens X+1
-        const int xlo = 2 * (blockIdx.y * a.tx) - 1;
-        if (x != xlo) {
-          acc.x = fma(0.5, rs.x, acc.x);
-          acc.y = fma(0.5, rs.y, acc.y);
-          const int X = (x - 1) >> 1, Y = yt >> 1;
-          if (live && Y <= a.gc.ny) a.out0[a.gc.idx(X, Y)] = make_double2(0.25 * acc.x, 0.25 * acc.y);
-        }
-        acc = make_double2(0.5 * rs.x, 0.5 * rs.y);
+    if ((x & 1) == 0) {  // fine column 2X: weight 1
+      acc.x += r.x;
+      acc.y += r.y;
+      return;
+    }
+    // fine column 2X+1 closes coarse column X = (x-1)/2 and opens X+1
+    const int xlo = 2 * (blockIdx.y * a.tx) - 1;
+    if (x != xlo) {
+      acc.x = fma(0.5, r.x, acc.x);
+      acc.y = fma(0.5, r.y, acc.y);
+      const int X = (x - 1) >> 1;
+      double2* buf = rbuf[X & 1];
+      buf[t] = acc;
+      consumer_sync();
+      // even fine rows (odd t) carry the coarse rows
+      if ((t & 1) && t < kTY - 1) {
+        const double2 m = buf[t - 1], p = buf[t + 1];
+        const int Y = yt >> 1;
+        if (live && Y <= a.gc.ny)
+          a.out0[a.gc.idx(X, Y)] = make_double2(0.25 * fma(0.5, m.x + p.x, acc.x), 0.25 * fma(0.5, m.y + p.y, acc.y));
       }
     }
+    acc = make_double2(0.5 * r.x, 0.5 * r.y);
   }
 };
 

@@ -19,7 +19,7 @@ import torch.multiprocessing as mp
 
 import paper_2301_07457_b200 as P
 
-GX = 2  # ghost columns per side (tmg_device.cuh kGX)
+GX = 3  # ghost columns per side (tmg_device.cuh kGX)
 
 
 def _free_port():
