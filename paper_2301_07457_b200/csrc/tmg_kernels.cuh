@@ -102,7 +102,10 @@ __device__ __forceinline__ void apply_scalar(RedOp op, double acc, PcgState* st,
       if (!(acc > 0.0) && st->status == 0) st->status = 4;
       st->beta = (st->it == 1) ? 0.0 : acc / st->zr_prev;
       st->zr_prev = acc;
-      if (hm) hm->zr = acc;
+      if (hm) {
+        hm->zr = acc;
+        hm->status = st->status;
+      }
       break;
     }
     case kRedPap: {
@@ -110,7 +113,10 @@ __device__ __forceinline__ void apply_scalar(RedOp op, double acc, PcgState* st,
       st->pap = acc;
       if (!(acc > 0.0) && st->status == 0) st->status = 3;
       st->alpha = st->zr / acc;
-      if (hm) hm->pap = acc;
+      if (hm) {
+        hm->pap = acc;
+        hm->status = st->status;
+      }
       break;
     }
     case kRedRr: {

@@ -60,13 +60,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// The suspend-time hint parks a waiting warp until the phase completes
+// instead of the short default limit: without it the producer warp spins on
+// its empty slots and takes issue slots from the consumer warps it shares a
+// scheduler with (ncu showed ~20% of a fine stage's instructions there).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)
       : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -95,6 +99,7 @@ struct MarchArgs {
   const double2* uc;  // coarse field (StProlongSweep)
   double2* out0;
   double2* out1;
+  double2* out2;      // StSweep01U: x (read and written, own rows)
   double omega;
   double* partials;
   unsigned* ticket;
@@ -371,19 +376,43 @@ struct StResidual : WithF<0> {
 // for the thread's own row (one division per node) and shared with the
 // neighbouring rows through a shared-memory column exchange; then
 // x2 = x1 + omega D^-1 (f - A x1). The streamed window field is f.
-struct StSweep01 {
-  static constexpr int NS = 3, kRow0 = 0, kOwned = kTY, kLead = 1;
+//
+// UPD additionally finishes the previous PCG iteration first (pcg_solve,
+// solvers.cpp:383-386): the window field is r_old with A p_old beside it,
+// f = r = r_old - alpha A p is formed wherever f is read, and the own rows
+// write r (out1) and x += alpha p (x in out2, p streamed from uc) and
+// reduce r.r. This moves the x/r update off its own 96-byte-per-node pass
+// into the (compute-bound) first smoothing pass.
+template <bool UPD>
+struct StSweep01T {
+  static constexpr int NS = UPD ? 6 : 3, kRow0 = 0, kOwned = kTY, kLead = 1;
   static constexpr int O_F = 0, O_E = O_F + sbytes(kTY + 2, 16), O_M = O_E + sbytes(kTY + 4, 8);
-  static constexpr int kSlot = O_M + sbytes(kTY + 2, 1);
+  static constexpr int O_A = O_M + sbytes(kTY + 2, 1);  // UPD: A p_old, window rows
+  static constexpr int O_X = O_A + sbytes(kTY + 2, 16);  // UPD: x, own rows
+  static constexpr int O_P = O_X + sbytes(kTY, 16);      // UPD: p_old, own rows
+  static constexpr int kSlot = UPD ? O_P + sbytes(kTY, 16) : O_A;
   __device__ static StreamDesc stream(const MarchArgs& a, int k) {
     if (k == 0) return {reinterpret_cast<const unsigned char*>(a.f), 16, -1, kTY + 2, false};
     if (k == 1) return {reinterpret_cast<const unsigned char*>(a.E), 8, -2, kTY + 4, false};
-    return {reinterpret_cast<const unsigned char*>(a.M), 1, -1, kTY + 2, false};
+    if (k == 2) return {reinterpret_cast<const unsigned char*>(a.M), 1, -1, kTY + 2, false};
+    if (k == 3) return {reinterpret_cast<const unsigned char*>(a.u2), 16, -1, kTY + 2, false};
+    if (k == 4) return {reinterpret_cast<const unsigned char*>(a.out2), 16, 0, kTY, false};
+    return {reinterpret_cast<const unsigned char*>(a.uc), 16, 0, kTY, false};
   }
-  __device__ static int off(int k) { return k == 0 ? O_F : (k == 1 ? O_E : O_M); }
-  // x1 at stream row index j (row y0 - 1 + j) of column c; *w = omega / D
+  __device__ static int off(int k) {
+    return k == 0 ? O_F : (k == 1 ? O_E : (k == 2 ? O_M : (k == 3 ? O_A : (k == 4 ? O_X : O_P))));
+  }
+  // f at stream row index j (row y0 - 1 + j); UPD: r_old - alpha A p_old
+  // (the same fma as k_update_xr, so r is bit-identical to the unfused path)
+  __device__ static double2 f_at(const unsigned char* s, const int* mis, int j, double alpha) {
+    const double2 r = sat<double2>(s, O_F, mis[0], j);
+    if (!UPD) return r;
+    const double2 q = sat<double2>(s, O_A, mis[3], j);
+    return make_double2(fma(-alpha, q.x, r.x), fma(-alpha, q.y, r.y));
+  }
+  // x1 at stream row index j of column c; *w = omega / D
   __device__ static double2 x1_at(const MarchArgs& a, const unsigned char* s, const unsigned char* ps,
-                                  const int* mis, int j, double2* w) {
+                                  const int* mis, int j, double alpha, double2* w) {
     // node rows r = y0-1+j: elements (c-1, r-1), (c, r-1), (c, r), (c-1, r)
     // sit at E-stream indices j and j+1 (stream starts at row y0-2)
     const double eA = ps ? sat<double>(ps, O_E, mis[1], j) : 0.0;
@@ -391,12 +420,12 @@ struct StSweep01 {
     const double eB = sat<double>(s, O_E, mis[1], j), eC = sat<double>(s, O_E, mis[1], j + 1);
     const uint32_t m = *(s + O_M + mis[2] + j);
     const double2 d = fine_diag(eA, eB, eC, eD, m);
-    const double2 f = sat<double2>(s, O_F, mis[0], j);
     // ghost nodes have no elements: D = 0 and x1 = 0
     if (d.x == 0.0) {
       if (w) *w = make_double2(0.0, 0.0);
       return make_double2(0.0, 0.0);
     }
+    const double2 f = f_at(s, mis, j, alpha);
     const double s0 = a.omega * rcp_nr(d.x);
     const double s1 = (d.y == d.x) ? s0 : a.omega * rcp_nr(d.y);
     if (w) *w = make_double2(s0, s1);
@@ -408,10 +437,11 @@ struct StSweep01 {
   __device__ static void load(const MarchArgs& a, const unsigned char* s, const unsigned char* ps,
                               const int* mis, int t, int c, Col& col) {
     __shared__ double2 xb[2][kTY + 2];
+    const double alpha = UPD ? a.st->alpha : 0.0;
     double2* buf = xb[c & 1];
-    buf[t + 1] = x1_at(a, s, ps, mis, t + 1, &col.w);
-    if (t == 0) buf[0] = x1_at(a, s, ps, mis, 0, nullptr);
-    if (t == kTY - 1) buf[kTY + 1] = x1_at(a, s, ps, mis, kTY + 1, nullptr);
+    buf[t + 1] = x1_at(a, s, ps, mis, t + 1, alpha, &col.w);
+    if (t == 0) buf[0] = x1_at(a, s, ps, mis, 0, alpha, nullptr);
+    if (t == kTY - 1) buf[kTY + 1] = x1_at(a, s, ps, mis, kTY + 1, alpha, nullptr);
     consumer_sync();
     col.u[0] = buf[t];
     col.u[1] = buf[t + 1];
@@ -421,16 +451,27 @@ struct StSweep01 {
     col.m3 = mask3(s, O_M, mis[2], t);
   }
   __device__ static void run(const MarchArgs& a, const Col& L, const Col& C, const Col& R,
-                             const unsigned char* cs, const int* mis, int x, int yt, int t, bool live, double&,
+                             const unsigned char* cs, const int* mis, int x, int yt, int t, bool live, double& part,
                              double2&) {
     if (!live) return;
     double2 y, d;
     window_apply(L, C, R, y, d);
-    const double2 f = sat<double2>(cs, O_F, mis[0], t + 1);
+    const double alpha = UPD ? a.st->alpha : 0.0;
+    const double2 f = f_at(cs, mis, t + 1, alpha);
     const double2 x1 = C.u[1];
-    a.out0[a.g.idx(x, yt)] = make_double2(fma(C.w.x, f.x - y.x, x1.x), fma(C.w.y, f.y - y.y, x1.y));
+    const long i = a.g.idx(x, yt);
+    a.out0[i] = make_double2(fma(C.w.x, f.x - y.x, x1.x), fma(C.w.y, f.y - y.y, x1.y));
+    if (UPD) {
+      a.out1[i] = f;
+      const double2 xo = sat<double2>(cs, O_X, mis[4], t), pp = sat<double2>(cs, O_P, mis[5], t);
+      a.out2[i] = make_double2(fma(alpha, pp.x, xo.x), fma(alpha, pp.y, xo.y));
+      part = fma(f.x, f.x, part);
+      part = fma(f.y, f.y, part);
+    }
   }
 };
+using StSweep01 = StSweep01T<false>;
+using StSweep01U = StSweep01T<true>;
 
 // f_c = (1/4) P^T (f - A u) in one pass. Thread t owns fine row
 // yt = y0 - 1 + t so the 63 coarse rows Y = y0/2 .. y0/2 + 62 see their three

@@ -27,6 +27,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "tmg_device.cuh"
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
   __shared__ uint64_t full[kSStages], empty[kSStages];
   __shared__ double2 xa[3][kSY + 2];  // stage-A input columns (x1 / w)
   __shared__ double2 xb[3][kSY + 2];  // stage-B input columns (x2 / x3)
-  __shared__ double2 rb[2][kSY];      // DOWN: residual rows for the restriction
+  __shared__ double2 rb[3][kSY];      // DOWN: residual rows for the restriction
   constexpr int kSlot = UP ? kSSlotUp : kSSlotDown;
 
   const Grid& g = a.g;
@@ -243,56 +244,63 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
     return make_double2(xv.x + pu.x, xv.y + pu.y);
   };
 
-  // rotating windows: A over stage-A inputs, B over stage-B inputs
+  // rotating windows: A over stage-A inputs, B over stage-B inputs. The
+  // entry loop is unrolled by 3 so the windows (and the smem exchange
+  // buffers) rotate by compile-time index instead of register moves: at
+  // phase P the window columns x-1 / x / x+1 are w[P] / w[P+1] / w[P+2]
+  // (mod 3), w[P+2] being the column entered this step.
   double2 wa[3][3], wb[3][3];
 #pragma unroll
   for (int p = 0; p < 3; ++p)
 #pragma unroll
     for (int q = 0; q < 3; ++q) wa[p][q] = wb[p][q] = make_double2(0.0, 0.0);
 
-  for (int e = 0; e < nent; ++e) {
+  // ring position of entry e (slot index, mbarrier phase) and the slots of
+  // entries e-1 .. e-3, advanced incrementally
+  int si = 0;
+  uint32_t ph = 0;
+  const unsigned char* sp1 = nullptr;
+  const unsigned char* sp2 = nullptr;
+  const unsigned char* sp3 = nullptr;
+  int srel = kSStages - 3;  // slot of entry e-3 (mod kSStages)
+
+  auto step = [&](auto phase, int e) {
+    constexpr int P = decltype(phase)::value;
+    constexpr int IL = P, IC = (P + 1) % 3, IR = (P + 2) % 3;
     const int c = cf + e;
-    mbar_wait(&full[e % kSStages], (e / kSStages) & 1);
-    const unsigned char* s0 = slot(e);
+    mbar_wait(&full[si], ph);
+    const unsigned char* s0 = smem_raw + static_cast<size_t>(si) * kSlot;
     const bool have0 = in_storage(c);
-    const unsigned char* s1 = (e >= 1 && in_storage(c - 1)) ? slot(e - 1) : nullptr;
-    const unsigned char* s2 = (e >= 2 && in_storage(c - 2)) ? slot(e - 2) : nullptr;
-    const unsigned char* s3 = (e >= 3 && in_storage(c - 3)) ? slot(e - 3) : nullptr;
+    const unsigned char* s1 = (e >= 1 && in_storage(c - 1)) ? sp1 : nullptr;
+    const unsigned char* s2 = (e >= 2 && in_storage(c - 2)) ? sp2 : nullptr;
+    const unsigned char* s3 = (e >= 3 && in_storage(c - 3)) ? sp3 : nullptr;
     // (1) stage-A inputs of column c
     {
-      double2* buf = xa[(c + 3) % 3];
+      double2* buf = xa[P];
       buf[t + 1] = have0 ? a_in(s0, s1, c, j) : make_double2(0.0, 0.0);
       if (t == 0) buf[0] = have0 ? a_in(s0, s1, c, 0) : make_double2(0.0, 0.0);
       if (t == kSY - 1) buf[kSY + 1] = have0 ? a_in(s0, s1, c, kSY + 1) : make_double2(0.0, 0.0);
       s_consumer_sync();
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        wa[0][q] = wa[1][q];
-        wa[1][q] = wa[2][q];
-        wa[2][q] = buf[t + q];
-      }
+      for (int q = 0; q < 3; ++q) wa[IR][q] = buf[t + q];
     }
     // (2) stage A at column c-1
     {
       double2 v = make_double2(0.0, 0.0);
       if (e >= 1 && s1 && s2 && inside(c - 1, yt)) {
         double2 y, d;
-        s_apply(SPlanes{s1, misS}, SPlanes{s2, misS}, j, wa[0], wa[1], wa[2], y, d);
-        v = s_jacobi(wa[1][1], fat(s1, j), y, d, a.omega);
+        s_apply(SPlanes{s1, misS}, SPlanes{s2, misS}, j, wa[IL], wa[IC], wa[IR], y, d);
+        v = s_jacobi(wa[IC][1], fat(s1, j), y, d, a.omega);
         // x2 of the nodes this CTA owns: rows [y0, y0+kOwned), fine columns
         // [2 X0, 2 X1) of its coarse columns
         if (!UP && t >= 2 && t < 2 + kOwned && c - 1 > xlo && c - 1 <= xhi && c - 1 < g.ncol && yt <= g.ny)
           a.out[g.idx(c - 1, yt)] = v;
       }
-      double2* buf = xb[(c + 2) % 3];
+      double2* buf = xb[P];
       buf[t + 1] = v;
       s_consumer_sync();
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        wb[0][q] = wb[1][q];
-        wb[1][q] = wb[2][q];
-        wb[2][q] = (t >= 1 && t < kSY - 1) ? buf[t + q] : make_double2(0.0, 0.0);
-      }
+      for (int q = 0; q < 3; ++q) wb[IR][q] = (t >= 1 && t < kSY - 1) ? buf[t + q] : make_double2(0.0, 0.0);
     }
     // (3) stage B at column c-2
     if (e >= 2) {
@@ -300,15 +308,15 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
       double2 out = make_double2(0.0, 0.0);
       if (t >= 1 && t < kSY - 1 && s2 && s3 && inside(x, yt)) {
         double2 y, d;
-        s_apply(SPlanes{s2, misS}, SPlanes{s3, misS}, j, wb[0], wb[1], wb[2], y, d);
+        s_apply(SPlanes{s2, misS}, SPlanes{s3, misS}, j, wb[IL], wb[IC], wb[IR], y, d);
         const double2 f = fat(s2, j);
-        out = UP ? s_jacobi(wb[1][1], f, y, d, a.omega) : make_double2(f.x - y.x, f.y - y.y);
+        out = UP ? s_jacobi(wb[IC][1], f, y, d, a.omega) : make_double2(f.x - y.x, f.y - y.y);
       }
       if (UP) {
         if (t >= 1 && t < kSY - 1 && x >= xlo && x <= xhi && yt <= g.ny) a.out[g.idx(x, yt)] = out;
       } else if (x >= xlo && x <= xhi) {
         // restriction: rows (1/2, 1, 1/2) around even fine rows, columns the same
-        double2* buf = rb[x & 1];
+        double2* buf = rb[P];
         buf[t] = out;
         s_consumer_sync();
         if ((yt & 1) == 0 && t >= 2 && t < kSY - 2) {
@@ -332,9 +340,27 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
     // (4) column c-3 is no longer needed
     if (e >= 3) {
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[(e - 3) % kSStages]);
+      if (lane == 0) mbar_arrive(&empty[srel]);
     }
+    // advance the ring position
+    sp3 = sp2;
+    sp2 = sp1;
+    sp1 = s0;
+    srel = (srel + 1 == kSStages) ? 0 : srel + 1;
+    if (++si == kSStages) {
+      si = 0;
+      ph ^= 1u;
+    }
+  };
+
+  int e = 0;
+  for (; e + 2 < nent; e += 3) {
+    step(std::integral_constant<int, 0>{}, e);
+    step(std::integral_constant<int, 1>{}, e + 1);
+    step(std::integral_constant<int, 2>{}, e + 2);
   }
+  if (e < nent) step(std::integral_constant<int, 0>{}, e);
+  if (e + 1 < nent) step(std::integral_constant<int, 1>{}, e + 1);
 }
 
 }  // namespace tmg

@@ -174,6 +174,28 @@ def test_warm_start_and_zero_rhs_and_max_iter():
     assert rel(short.solution, rs["solution"]) <= 1e-10
 
 
+@pytest.mark.parametrize("sweeps", [1, 2, 3])
+@pytest.mark.parametrize("max_iter", [1, 2, 5, 500])
+def test_sweep_counts_and_iteration_caps(sweeps, max_iter):
+    """pre = post = 1 takes the unfused x/r update; 2 and 3 finish each PCG
+    iteration inside the next one's first smoothing pass (and after the loop
+    when max_iter stops it): iterates, histories and caps must not tell."""
+    ops, sysc, b, _, _ = pair(64, 32, 3, seed=4)
+    rep = P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-8, max_iter=max_iter, pre_sweeps=sweeps,
+                                               post_sweeps=sweeps))
+    ref = sysc.solve(b, tol=1e-8, max_iter=max_iter, pre=sweeps, post=sweeps)
+    assert rep.converged == ref["converged"]
+    if not ref["converged"]:
+        assert rep.iterations == ref["iterations"] == max_iter
+        assert rel(rep.solution, ref["solution"]) <= 1e-10
+    else:
+        assert abs(rep.iterations - ref["iterations"]) <= 2
+        assert rel(rep.solution, ref["solution"]) <= 1e-8
+    assert len(rep.residual_history) == rep.iterations + 1
+    n = min(len(rep.residual_history), len(ref["residual_history"]))
+    np.testing.assert_allclose(rep.residual_history[:n], ref["residual_history"][:n], rtol=1e-6)
+
+
 def test_single_level_hierarchy_solves_in_one_iteration():
     """test_solvers.cpp:328-342 for the elasticity system."""
     ops, sysc, b, _, _ = pair(8, 8, 0)
