@@ -780,13 +780,13 @@ void launch_smarch(H* h, Rank& R, int l, const double2* x2, const double2* uc, d
   dim3 grid;
   size_t sm;
   if (!UP) {
-    sm = static_cast<size_t>(kSSlotDown) * kSStages;
+    sm = static_cast<size_t>(kSSlotDown) * s_stages<false>();
     const int slots = device_slots(reinterpret_cast<const void*>(k_smarch<false>), kSThreads, sm);
     const long ty = (a.gc.ny + 1 + (kSY - 4) / 2 - 1) / ((kSY - 4) / 2);
     a.tx = march_tx(ty, a.gc.ncol, slots, 2, 7);
     grid = dim3(ty, (a.gc.ncol + a.tx - 1) / a.tx);
   } else {
-    sm = static_cast<size_t>(kSSlotUp) * kSStages;
+    sm = static_cast<size_t>(kSSlotUp) * s_stages<true>();
     const int slots = device_slots(reinterpret_cast<const void*>(k_smarch<true>), kSThreads, sm);
     const long ty = (a.g.ny + 1 + (kSY - 2) - 1) / (kSY - 2);
     // even: CTA column ranges start on even columns
@@ -1346,9 +1346,9 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
   if (prop.major != 10) fail(TMG_ERR_CUDA, std::string("libtmg_gpu is built for sm_100a; device is ") + prop.name);
   CK(cudaSetDevice(device));
   CK(cudaFuncSetAttribute(k_smarch<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(kSSlotDown * kSStages)));
+                          static_cast<int>(kSSlotDown * s_stages<false>())));
   CK(cudaFuncSetAttribute(k_smarch<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(kSSlotUp * kSStages)));
+                          static_cast<int>(kSSlotUp * s_stages<true>())));
   CK(cudaFuncSetAttribute(k_march<StSweep01U, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(StSweep01U::kSlot * kStages)));
   CK(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking));

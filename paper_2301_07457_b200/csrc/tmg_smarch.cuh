@@ -38,7 +38,10 @@ namespace tmg {
 constexpr int kSY = 96;                 // consumer threads (rows) per CTA
 constexpr int kSWarps = kSY / 32;
 constexpr int kSThreads = kSY + 32;     // + one producer warp
-constexpr int kSStages = 5;             // 4 resident columns + 1 in flight
+// ring depth: 4 resident columns + 2 in flight, the most that keeps two
+// CTAs per SM
+template <bool UP>
+__host__ __device__ constexpr int s_stages() { return 6; }
 constexpr int kSRows = kSY + 2;         // streamed rows per column
 constexpr long kSMinNodes = 200000;     // smaller levels: one-pass kernels
 
@@ -55,13 +58,14 @@ struct SMarchArgs {
   double omega;
 };
 
-// Slot layout: planes [19][kSRows], then f, then (UP) x2 and coarse.
+// Slot layout: planes [19][kSRows], then f, then (UP) the coarse column. The
+// UP kernel's x2 is read by the threads directly (one column ahead) so that
+// six stages still fit two CTAs per SM.
 constexpr int kSPlane = sbytes(kSRows, 8);
 constexpr int kSO_F = kStencilPlanes * kSPlane;
-constexpr int kSO_X = kSO_F + sbytes(kSRows, 16);
-constexpr int kSO_C = kSO_X + sbytes(kSRows, 16);
+constexpr int kSO_C = kSO_F + sbytes(kSRows, 16);
 constexpr int kSCoarseRows = kSRows / 2 + 3;
-constexpr int kSSlotDown = kSO_X;
+constexpr int kSSlotDown = kSO_C;
 constexpr int kSSlotUp = kSO_C + sbytes(kSCoarseRows, 16);
 
 // 2x2-block stencil application at row j of the centre column (cs = its
@@ -88,21 +92,25 @@ __device__ __forceinline__ void s_bwd(const SPlanes& p, int k, int j, double2 v,
   y1 = fma(p.at(k + 3, j), v.y, y1);
 }
 
+// Three independent accumulator pairs (centre/N/SE, E/NE/S, NW/W/SW) keep
+// three FMA chains in flight per thread; with two resident CTAs a single
+// chain per dof left the FP64 pipe waiting on its own latency.
 __device__ __forceinline__ void s_apply(const SPlanes& C, const SPlanes& L, int j, const double2 (&l)[3],
                                         const double2 (&c)[3], const double2 (&r)[3], double2& y, double2& d) {
   const double c00 = C.at(0, j), c01 = C.at(1, j), c11 = C.at(2, j);
-  double y0 = c00 * c[1].x, y1 = c01 * c[1].x;
-  y0 = fma(c01, c[1].y, y0);
-  y1 = fma(c11, c[1].y, y1);
-  s_fwd(C, 3, j, c[2], y0, y1);    // N
-  s_fwd(C, 7, j, r[0], y0, y1);    // SE
-  s_fwd(C, 11, j, r[1], y0, y1);   // E
-  s_fwd(C, 15, j, r[2], y0, y1);   // NE
-  s_bwd(C, 3, j - 1, c[0], y0, y1);   // S  = N of (x, y-1)
-  s_bwd(L, 7, j + 1, l[2], y0, y1);   // NW = SE of (x-1, y+1)
-  s_bwd(L, 11, j, l[1], y0, y1);      // W  = E of (x-1, y)
-  s_bwd(L, 15, j - 1, l[0], y0, y1);  // SW = NE of (x-1, y-1)
-  y = make_double2(y0, y1);
+  double a0 = c00 * c[1].x, a1 = c01 * c[1].x;
+  a0 = fma(c01, c[1].y, a0);
+  a1 = fma(c11, c[1].y, a1);
+  double b0 = 0.0, b1 = 0.0, e0 = 0.0, e1 = 0.0;
+  s_fwd(C, 3, j, c[2], a0, a1);       // N
+  s_fwd(C, 11, j, r[1], b0, b1);      // E
+  s_bwd(L, 7, j + 1, l[2], e0, e1);   // NW = SE of (x-1, y+1)
+  s_fwd(C, 7, j, r[0], a0, a1);       // SE
+  s_fwd(C, 15, j, r[2], b0, b1);      // NE
+  s_bwd(L, 11, j, l[1], e0, e1);      // W  = E of (x-1, y)
+  s_bwd(C, 3, j - 1, c[0], b0, b1);   // S  = N of (x, y-1)
+  s_bwd(L, 15, j - 1, l[0], e0, e1);  // SW = NE of (x-1, y-1)
+  y = make_double2((a0 + b0) + e0, (a1 + b1) + e1);
   d = make_double2(c00, c11);
 }
 
@@ -120,10 +128,13 @@ __device__ __forceinline__ double2 s_jacobi(double2 x, double2 f, double2 y, dou
 template <bool UP>
 __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int kSStages = s_stages<UP>();
   __shared__ uint64_t full[kSStages], empty[kSStages];
-  __shared__ double2 xa[3][kSY + 2];  // stage-A input columns (x1 / w)
-  __shared__ double2 xb[3][kSY + 2];  // stage-B input columns (x2 / x3)
-  __shared__ double2 rb[3][kSY];      // DOWN: residual rows for the restriction
+  // row-exchange columns; one buffer each suffices: between a step's reads
+  // of a buffer and the next step's writes to it lies a consumer barrier
+  __shared__ double2 xa[kSY + 2];  // stage-A inputs (x1 / w)
+  __shared__ double2 xb[kSY + 2];  // stage-B inputs (x2 / x3)
+  __shared__ double2 rb[kSY];      // DOWN: residual rows for the restriction
   constexpr int kSlot = UP ? kSSlotUp : kSSlotDown;
 
   const Grid& g = a.g;
@@ -165,9 +176,8 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
   const uintptr_t pS = reinterpret_cast<uintptr_t>(a.S), pf = reinterpret_cast<uintptr_t>(a.f);
   const int misS = static_cast<int>((pS + static_cast<uintptr_t>(g.idx(0, y0 + r0)) * 8) & 15u);
   const int misF = static_cast<int>((pf + static_cast<uintptr_t>(g.idx(0, y0 + r0)) * 16) & 15u);
-  int misX = 0, misC = 0;
+  int misC = 0;
   if (UP) {
-    misX = static_cast<int>((reinterpret_cast<uintptr_t>(a.x2) + static_cast<uintptr_t>(g.idx(0, y0 + r0)) * 16) & 15u);
     misC = static_cast<int>((reinterpret_cast<uintptr_t>(a.uc) +
                              static_cast<uintptr_t>(a.gc.idx(0, (y0 >> 1) + cr0)) * 16) & 15u);
   }
@@ -176,9 +186,8 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
     if (t == kSY) {
       const uint32_t bp = (kSRows * 8 + misS + 15) / 16 * 16;
       const uint32_t bf = (kSRows * 16 + misF + 15) / 16 * 16;
-      const uint32_t bx = (kSRows * 16 + misX + 15) / 16 * 16;
       const uint32_t bc = (kSCoarseRows * 16 + misC + 15) / 16 * 16;
-      const uint32_t total = kStencilPlanes * bp + bf + (UP ? bx + bc : 0u);
+      const uint32_t total = kStencilPlanes * bp + bf + (UP ? bc : 0u);
       for (int j = 0; j < nent; ++j) {
         const int s = j % kSStages;
         if (j >= kSStages) mbar_wait(&empty[s], ((j / kSStages) - 1) & 1);
@@ -195,7 +204,6 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
                    &full[s]);
         bulk_g2s(sl + kSO_F, reinterpret_cast<const unsigned char*>(a.f + ri) - misF, bf, &full[s]);
         if (UP) {
-          bulk_g2s(sl + kSO_X, reinterpret_cast<const unsigned char*>(a.x2 + ri) - misX, bx, &full[s]);
           const long ci = a.gc.idx((c + 1) >> 1, (y0 >> 1) + cr0);
           bulk_g2s(sl + kSO_C, reinterpret_cast<const unsigned char*>(a.uc + ci) - misC, bc, &full[s]);
         }
@@ -214,7 +222,7 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
   };
   double2 acc = make_double2(0.0, 0.0);
   // stage-A input at stream row jj of column c (slot s, previous slot ps)
-  auto a_in = [&](const unsigned char* s, const unsigned char* ps, int c, int jj) -> double2 {
+  auto a_in = [&](const unsigned char* s, const unsigned char* ps, int c, int jj, double2 xv) -> double2 {
     const int y = y0 + r0 + jj;
     if (!inside(c, y)) return make_double2(0.0, 0.0);
     if (!UP) {
@@ -224,7 +232,6 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
     }
     // w = x2 + P u_c (bilinear, grid.cpp:20-46); coarse column ceil(c/2) in s,
     // floor(c/2) in ps for odd columns; coarse row index of fine row y
-    const double2 xv = *reinterpret_cast<const double2*>(s + kSO_X + misX + jj * 16);
     const int gy = y - 2 * ((y0 >> 1) + cr0);  // fine row relative to the coarse stream start
     auto crow = [&](const unsigned char* sl, int k) {
       return *reinterpret_cast<const double2*>(sl + kSO_C + misC + k * 16);
@@ -243,6 +250,19 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
     }
     return make_double2(xv.x + pu.x, xv.y + pu.y);
   };
+
+  // UP: x2 of the own row (and of the halo row of threads 0 / kSY-1) for
+  // the next column, loaded while the current one is processed
+  double2 x2o = make_double2(0.0, 0.0), x2h = make_double2(0.0, 0.0);
+  auto fetch_x2 = [&](int c) {
+    const int yo = y0 + r0 + j;
+    x2o = inside(c, yo) ? a.x2[g.idx(c, yo)] : make_double2(0.0, 0.0);
+    if (t == 0 || t == kSY - 1) {
+      const int yh = y0 + r0 + (t == 0 ? 0 : kSY + 1);
+      x2h = inside(c, yh) ? a.x2[g.idx(c, yh)] : make_double2(0.0, 0.0);
+    }
+  };
+  if (UP) fetch_x2(cf);
 
   // rotating windows: A over stage-A inputs, B over stage-B inputs. The
   // entry loop is unrolled by 3 so the windows (and the smem exchange
@@ -276,10 +296,12 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
     const unsigned char* s3 = (e >= 3 && in_storage(c - 3)) ? sp3 : nullptr;
     // (1) stage-A inputs of column c
     {
-      double2* buf = xa[P];
-      buf[t + 1] = have0 ? a_in(s0, s1, c, j) : make_double2(0.0, 0.0);
-      if (t == 0) buf[0] = have0 ? a_in(s0, s1, c, 0) : make_double2(0.0, 0.0);
-      if (t == kSY - 1) buf[kSY + 1] = have0 ? a_in(s0, s1, c, kSY + 1) : make_double2(0.0, 0.0);
+      double2* buf = xa;
+      const double2 xo = x2o, xh = x2h;
+      if (UP && e + 1 < nent) fetch_x2(c + 1);
+      buf[t + 1] = have0 ? a_in(s0, s1, c, j, xo) : make_double2(0.0, 0.0);
+      if (t == 0) buf[0] = have0 ? a_in(s0, s1, c, 0, xh) : make_double2(0.0, 0.0);
+      if (t == kSY - 1) buf[kSY + 1] = have0 ? a_in(s0, s1, c, kSY + 1, xh) : make_double2(0.0, 0.0);
       s_consumer_sync();
 #pragma unroll
       for (int q = 0; q < 3; ++q) wa[IR][q] = buf[t + q];
@@ -296,7 +318,7 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
         if (!UP && t >= 2 && t < 2 + kOwned && c - 1 > xlo && c - 1 <= xhi && c - 1 < g.ncol && yt <= g.ny)
           a.out[g.idx(c - 1, yt)] = v;
       }
-      double2* buf = xb[P];
+      double2* buf = xb;
       buf[t + 1] = v;
       s_consumer_sync();
 #pragma unroll
@@ -316,7 +338,7 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
         if (t >= 1 && t < kSY - 1 && x >= xlo && x <= xhi && yt <= g.ny) a.out[g.idx(x, yt)] = out;
       } else if (x >= xlo && x <= xhi) {
         // restriction: rows (1/2, 1, 1/2) around even fine rows, columns the same
-        double2* buf = rb[P];
+        double2* buf = rb;
         buf[t] = out;
         s_consumer_sync();
         if ((yt & 1) == 0 && t >= 2 && t < kSY - 2) {
