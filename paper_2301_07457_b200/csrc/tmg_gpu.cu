@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -334,6 +335,9 @@ struct tmg_gpu_handle {
   long graph_kernels[3] = {0, 0, 0};
   int g_gamma = -1, g_pre = -1, g_post = -1;
   bool g_fused = false;
+  // coarse levels at least this large use the two-stage kernels
+  // (TMG_SMARCH_MIN_NODES overrides it, for tests on small meshes)
+  long smarch_min_nodes = kSMinNodes;
   // instrumentation
   long launches = 0;
   bool capturing = false;
@@ -858,7 +862,7 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
   }
   bool restricted = false;
   // the two-stage kernels pay off once a level streams more than it waits
-  const bool big = static_cast<long>(rs[0]->lev[l].g.ncol) * (rs[0]->lev[l].g.ny + 1) >= kSMinNodes;
+  const bool big = static_cast<long>(rs[0]->lev[l].g.ncol) * (rs[0]->lev[l].g.ny + 1) >= h->smarch_min_nodes;
   if (!fine && big && zero && pre == 2) {
     // coarse level: both pre-sweeps, the residual and the restriction in one
     // pass over the stencil (tmg_smarch.cuh)
@@ -899,7 +903,9 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
   const int visits = fine ? 1 : gamma;
   for (int t = 0; t < visits; ++t) enqueue_cycle(h, l - 1, t == 0, gamma, pre, post);
   auto ccur = [&](Rank& R) { return R.lev[l - 1].u[R.lev[l - 1].cur]; };
-  if (cdist) halo_vec(h, l - 1, ccur);
+  // the two-stage UP pass prolongates onto two ghost columns on the right:
+  // column ncol+1 interpolates coarse columns ncol/2 and ncol/2 + 1
+  if (cdist) halo_vec(h, l - 1, ccur, 1, 2);
   int p = 0;
   if (!fine && big && !zero && post == 2) {
     // coarse level: prolongation + both post-sweeps in one pass
@@ -1352,6 +1358,7 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
   CK(cudaFuncSetAttribute(k_march<StSweep01U, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(StSweep01U::kSlot * kStages)));
   CK(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking));
+  if (const char* v = std::getenv("TMG_SMARCH_MIN_NODES")) hp->smarch_min_nodes = std::atol(v);
   for (cudaEvent_t& e : hp->ev) CK(cudaEventCreate(&e));
   for (int i = 0; i < nlocal; ++i) {
     hp->own.push_back(std::make_unique<Rank>());
@@ -1736,13 +1743,16 @@ int tmg_gpu_vcycle(tmg_gpu_handle* h, const double* f, double* u, int gamma, int
   return guarded(h, [&] {
     need_setup(h);
     const int nc = h->nc;
+    // a zero start takes the zero-start passes, as inside pcgmg
+    const long n = 2L * (h->nx + 1) * (h->ny + 1);
+    const bool zero = std::all_of(u, u + n, [](double v) { return v == 0.0; });
     for (Rank* R : h->ranks) {
       for (Level& L : R->lev) L.cur = 0;
       upload_nodes(h->stream, R->r, f, R->fine().g);
       upload_nodes(h->stream, R->fine().u[0], u, R->fine().g);
     }
     halo_vec(h, nc, [&](Rank& R) { return R.r; });
-    enqueue_cycle(h, nc, false, gamma, pre_sweeps, post_sweeps);
+    enqueue_cycle(h, nc, zero, gamma, pre_sweeps, post_sweeps);
     for (Rank* R : h->ranks) download_nodes(h->stream, u, R->fine().u[R->fine().cur], R->fine().g);
     CK(cudaStreamSynchronize(h->stream));
   });

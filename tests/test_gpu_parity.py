@@ -196,6 +196,24 @@ def test_sweep_counts_and_iteration_caps(sweeps, max_iter):
     np.testing.assert_allclose(rep.residual_history[:n], ref["residual_history"][:n], rtol=1e-6)
 
 
+@pytest.mark.parametrize("nx,ny,nc", [(64, 64, 3), (128, 64, 4)])
+def test_two_stage_coarse_passes_match_reference(monkeypatch, nx, ny, nc):
+    """Small meshes normally keep the one-pass coarse kernels; lifting the
+    size threshold runs the two-stage ones (tmg_smarch.cuh) on every coarse
+    level, against the reference hierarchy."""
+    monkeypatch.setenv("TMG_SMARCH_MIN_NODES", "0")
+    ops, sysc, b, _, _ = pair(nx, ny, nc, seed=7)
+    rng = np.random.default_rng(8)
+    f = rng.standard_normal(b.size)
+    u = P.mg_cycle(ops, np.zeros_like(f), f, 1, 2, 2)
+    want = sysc.vcycle(f, np.zeros_like(f), 1, 2, 2)
+    assert rel(u, want) <= 1e-11
+    rep = P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-8, max_iter=500))
+    ref = sysc.solve(b, tol=1e-8, max_iter=500)
+    assert abs(rep.iterations - ref["iterations"]) <= 2
+    assert rel(rep.solution, ref["solution"]) <= 1e-8
+
+
 def test_single_level_hierarchy_solves_in_one_iteration():
     """test_solvers.cpp:328-342 for the elasticity system."""
     ops, sysc, b, _, _ = pair(8, 8, 0)

@@ -62,6 +62,28 @@ def test_slab_cycle_matches_single_rank(gamma, sweeps):
         assert rel(b, a) <= 1e-12
 
 
+@pytest.mark.parametrize("zero", [True, False])
+def test_two_stage_passes_on_slabs(monkeypatch, zero):
+    """With the size threshold lifted every coarse level runs the two-stage
+    passes (tmg_smarch.cuh), which read two ghost columns of their inputs and
+    of the coarse correction; a zero start takes them, as inside pcgmg."""
+    monkeypatch.setenv("TMG_SMARCH_MIN_NODES", "0")
+    nx, ny, nc = 128, 64, 4
+    one, _, _, _ = build(nx, ny, nc, 1)
+    for slabs, rep in ((2, 1), (3, 1), (4, 2), (2, 3)):
+        many, _, _, _ = build(nx, ny, nc, slabs, rep)
+        rng = np.random.default_rng(5)
+        f = rng.standard_normal(2 * (nx + 1) * (ny + 1))
+        u0 = np.zeros_like(f) if zero else rng.standard_normal(f.size)
+        a = P.mg_cycle(one, u0, f, 1, 2, 2)
+        b = P.mg_cycle(many, u0, f, 1, 2, 2)
+        assert rel(b, a) <= 1e-12, (slabs, rep)
+        cfg = P.SolverConfig(tol=1e-8, max_iter=500)
+        s1, sn = P.pcgmg_solve(one, a, cfg), P.pcgmg_solve(many, a, cfg)
+        assert sn.iterations == s1.iterations
+        np.testing.assert_allclose(sn.residual_history, s1.residual_history, rtol=1e-9)
+
+
 def test_slab_warm_start_and_determinism():
     nx, ny, nc = 128, 64, 4
     many, E, bc, b = build(nx, ny, nc, 2, 2)
