@@ -194,8 +194,10 @@ void* tmg_gpu_stream(tmg_gpu_handle* h);
 long tmg_gpu_launch_count(tmg_gpu_handle* h);
 /* Times `reps` back-to-back launches of one fine-level kernel on resident
  * data with CUDA events on the handle's stream. which: 0 = K.u apply,
- * 1 = damped-Jacobi sweep. *avg_ms = mean launch duration, *bytes = the
- * kernel's algorithmic bytes per launch. */
+ * 1 = damped-Jacobi sweep, 2 = the fused PCG update + two pre-sweeps (the
+ * solve's dominant pass; scratch outputs, needs a prior solve). *avg_ms =
+ * mean launch duration, *bytes = the kernel's algorithmic bytes per launch
+ * (DESIGN.md). */
 int tmg_gpu_time_kernel(tmg_gpu_handle* h, int which, int reps, double* avg_ms,
                         double* bytes);
 /* Breakdown of the last resident solve: setup ms, pcg ms (device events). */

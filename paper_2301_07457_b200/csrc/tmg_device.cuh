@@ -1,18 +1,21 @@
 // Device-side data layout and operator "providers" of the pCGMG path.
 //
 // HBM layout:
-//  * Every level stores its node field padded with a one-node ghost ring:
-//    node (x, y), x in [-1, nx+1], y in [-1, ny+1], lives at
-//        idx(x, y) = (x + 1) * P + y + OY
+//  * Every level stores its node field column-major with padding: a rank's
+//    slab of node columns [x0, x0 + ncol) (the whole mesh on one GPU) is
+//    stored as local columns 0 .. ncol-1 plus kGX ghost columns per side;
+//    local node (x, y), x in [-kGX, ncol + kGX), lives at
+//        idx(x, y) = (x + kGX) * P + y + OY
 //    with OY = 8 (so the interior of every column starts 128-byte aligned)
-//    and the pitch P a multiple of 8 nodes. Columns are contiguous in y,
+//    and the pitch P a multiple of 16 nodes. Columns are contiguous in y,
 //    exactly like the reference numbering x*(ny+1)+y (grid.hpp:19), so a
 //    host vector is one cudaMemcpy2D away.
 //  * A displacement field is double2 per node (u, v) = dofs (2n, 2n+1) of
 //    the reference (grid.hpp:20-22): one 16-byte vector load per node.
-//  * Ghost entries are zero in every array and no kernel writes them, so
-//    stencils need no boundary branches: a ghost element has modulus 0, a
-//    ghost node has value 0 and a zero stencil.
+//  * Entries outside the mesh are zero in every array and no kernel writes
+//    them, so stencils need no boundary branches: an element outside has
+//    modulus 0, a node outside has value 0 and a zero stencil. Ghost columns
+//    between slabs hold the neighbour's halo.
 //  * Fine level (matrix-free): per-element modulus E (8 B, same padded
 //    indexing, element (ex, ey) at idx(ex, ey)), per-node Dirichlet byte
 //    (low nibble: times dof 2n is listed fixed, high nibble: dof 2n+1), and

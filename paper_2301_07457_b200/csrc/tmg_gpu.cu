@@ -1818,9 +1818,26 @@ int tmg_gpu_time_kernel(tmg_gpu_handle* h, int which, int reps, double* avg_ms, 
     Rank& R = *h->ranks[0];
     Level& F = R.fine();
     const double nodes = static_cast<double>(F.g.ncol) * (F.g.ny + 1);
+    if (which < 0 || which > 2) fail(TMG_ERR_DIMENSION, "time_kernel: which must be 0, 1 or 2");
     auto launch = [&] {
-      if (which == 0) apply_level(h, R, h->nc, R.pbuf[0], R.ap);
-      else sweep_level(h, R, h->nc, false, F.u[0], F.u[1], R.r);
+      if (which == 0) {
+        apply_level(h, R, h->nc, R.pbuf[0], R.ap);
+      } else if (which == 1) {
+        sweep_level(h, R, h->nc, false, F.u[0], F.u[1], R.r);
+      } else {
+        // the fused PCG update + two sweeps as the solve runs it, on scratch
+        // outputs (the iterate stays untouched) with a plain reduction
+        MarchArgs a = march_args(h, R, nullptr);
+        a.f = R.r;
+        a.u2 = R.ap;
+        a.uc = R.pbuf[0];
+        a.out2 = F.res;
+        a.out1 = R.r2;
+        a.out0 = F.u[1];
+        a.rop = kRedPlain;
+        a.red_out = R.scal;
+        launch_march<StSweep01U, true>(h, a);
+      }
     };
     for (int w = 0; w < 3; ++w) launch();
     CK(cudaEventRecord(h->ev[2], h->stream));
@@ -1830,9 +1847,11 @@ int tmg_gpu_time_kernel(tmg_gpu_handle* h, int which, int reps, double* avg_ms, 
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]));
     *avg_ms = ms / reps;
-    // algorithmic bytes per node: apply reads u 16 + E 8 + mask 1, writes 16;
-    // the sweep additionally reads f 16
-    *bytes = nodes * (which == 0 ? 41.0 : 57.0);
+    // algorithmic bytes per node: apply reads u 16 +
+    // E 8 + mask 1, writes 16; the sweep additionally reads f 16; the fused
+    // update + two sweeps reads r_old, A p, x, p (16 each), E 8, mask 1 and
+    // writes r, x, x2 (16 each)
+    *bytes = nodes * (which == 0 ? 41.0 : (which == 1 ? 57.0 : 121.0));
   });
 }
 

@@ -15,10 +15,10 @@ for r in rows:
         data.append(dict(zip(hdr, r)))
 agg = collections.OrderedDict()
 tot = 0.0
-scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
 for d in data:
     name = d["Kernel Name"].split("(")[0][:48]
-    t = float(d["Metric Value"]) * scale.get(d["Metric Unit"], 1.0)
+    t = float(d["Metric Value"].replace(",", "")) * scale[d["Metric Unit"]]
     key = (name, d.get("Grid Size", ""))
     agg.setdefault(key, [0, 0.0])
     agg[key][0] += 1
