@@ -759,9 +759,9 @@ void prolong_level(H* h, Rank& R, int l, const double2* uc, double2* x, bool add
 }
 
 void coarse_solve(H* h, Rank& R, const double2* f, double2* u) {
-  const int nodes = R.n0 / 2;
-  const int nt = 256;
-  k_coarse_solve<<<(nodes + nt - 1) / nt, nt, sizeof(double) * R.n0, h->stream>>>(R.Ainv, R.n0, R.lev[0].g, f, u);
+  const int warps = R.n0 / 2, per_block = kCoarseSolveThreads / 32;
+  k_coarse_solve<<<(warps + per_block - 1) / per_block, kCoarseSolveThreads, sizeof(double) * R.n0, h->stream>>>(
+      R.Ainv, R.n0, R.lev[0].g, f, u);
   CKL();
   h->count();
 }

@@ -456,26 +456,36 @@ __global__ void k_gram(const double* __restrict__ LiT, double* __restrict__ Ainv
 }
 
 // u0 = A0^-1 f0 on the coarsest grid (CholeskyFactor::solve, solvers.cpp:154).
-__global__ void k_coarse_solve(const double* __restrict__ Ainv, int n, Grid g,
-                               const double2* __restrict__ f, double2* __restrict__ u) {
+// One warp per node: lanes stride over the input dofs (staged in smem) and
+// the warp sums its partials. A thread-per-node loop over all n inputs was a
+// 40 us latency chain per V-cycle at n = 162.
+constexpr int kCoarseSolveThreads = 256;
+__global__ void __launch_bounds__(kCoarseSolveThreads) k_coarse_solve(const double* __restrict__ Ainv, int n,
+                                                                      Grid g, const double2* __restrict__ f,
+                                                                      double2* __restrict__ u) {
   extern __shared__ double fd[];
-  for (int k = threadIdx.x; k < n / 2; k += blockDim.x) {
-    const int x = k / (g.ny + 1), y = k % (g.ny + 1);
-    const double2 v = f[g.idx(x, y)];
+  const int rows = g.ny + 1, nodes = n / 2;
+  for (int k = threadIdx.x; k < nodes; k += blockDim.x) {
+    const double2 v = f[g.idx(k / rows, k % rows)];
     fd[2 * k] = v.x;
     fd[2 * k + 1] = v.y;
   }
   __syncthreads();
-  const int node = blockIdx.x * blockDim.x + threadIdx.x;
-  if (node >= n / 2) return;
+  const int lane = threadIdx.x & 31;
+  const int node = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (node >= nodes) return;
   double s0 = 0.0, s1 = 0.0;
-  for (int k = 0; k < n; ++k) {
+  for (int k = lane; k < n; k += 32) {
     const double fk = fd[k];
     s0 = fma(Ainv[static_cast<long>(k) * n + 2 * node], fk, s0);
     s1 = fma(Ainv[static_cast<long>(k) * n + 2 * node + 1], fk, s1);
   }
-  const int x = node / (g.ny + 1), y = node % (g.ny + 1);
-  u[g.idx(x, y)] = make_double2(s0, s1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  if (lane == 0) u[g.idx(node / rows, node % rows)] = make_double2(s0, s1);
 }
 
 // --------------------------------------------------- PCG vector ops (K8) --
