@@ -166,6 +166,20 @@ int tmg_gpu_sensitivities(tmg_gpu_handle* h, const double* u, int nphases,
 int tmg_gpu_filter(tmg_gpu_handle* h, int nphases, const double* alpha, int phase,
                    double radius, const double* raw, double* out);
 
+/* One OC exchange between phases a and b of the element-major density
+ * alpha[e * nphases + phase] (host, updated in place), replacing
+ * oc_update_pair (mto.cpp:142-227, mto.hpp:73-77): move[e] is the element's
+ * move limit, floor_eps the density floor (DensityField::floor_eps). The
+ * bisection for the volume multiplier runs on the device with deterministic
+ * reductions. TMG_ERR_MULTIPLIER (alpha unchanged) when the target is missed
+ * after 101 steps, TMG_ERR_CONFIG for phase_a == phase_b. Single-rank
+ * handles. */
+int tmg_gpu_oc_update_pair(tmg_gpu_handle* h, double* alpha, int nphases, double floor_eps,
+                           int phase_a, int phase_b, const double* sens_a, const double* sens_b,
+                           double target, const double* move, double damping);
+/* Device time (ms) and bisection steps of the last tmg_gpu_oc_update_pair. */
+int tmg_gpu_oc_timings(tmg_gpu_handle* h, double* device_ms, int* steps);
+
 /* ---- kernel-level entry points (parity tests, profiling) --------------- */
 
 /* y = A_level x (SparseSymMatrix::multiply on ops.matrices[level],

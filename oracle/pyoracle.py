@@ -217,3 +217,19 @@ def filter_sensitivities(kind, nx, ny, alpha, phase, radius, raw):
     out = np.empty(nx * ny)
     getattr(lib(kind), kind + "_filter")(nx, ny, a.shape[1], _d(a), phase, radius, _d(raw), _d(out))
     return out
+
+
+def oc_update_pair(kind, alpha, phase_a, phase_b, sens_a, sens_b, target, move, damping, floor_eps=1e-3):
+    """One OC exchange (mto.cpp:142-227) on a copy of the element-major density
+    alpha [ne, nphases]; returns (new alpha, status) -- status 8 is the
+    reference's MultiplierError (alpha is then unchanged)."""
+    a = np.array(alpha, dtype=np.float64, copy=True, order="C")
+    ne, nph = a.shape
+    sa = np.ascontiguousarray(sens_a, dtype=np.float64)
+    sb = np.ascontiguousarray(sens_b, dtype=np.float64)
+    mv = np.ascontiguousarray(np.broadcast_to(np.asarray(move, dtype=np.float64), (ne,)))
+    f = getattr(lib(kind), kind + "_oc_update_pair")
+    f.restype = C.c_int
+    f.argtypes = [C.c_long, C.c_int, C.c_double, _D, C.c_int, C.c_int, _D, _D, C.c_double, _D, C.c_double]
+    st = f(ne, nph, floor_eps, _d(a), phase_a, phase_b, _d(sa), _d(sb), target, _d(mv), damping)
+    return a, st

@@ -313,4 +313,20 @@ int ref_filter(int nx, int ny, int nphases, const double* alpha, int phase,
   }
 }
 
+int ref_oc_update_pair(long ne, int nphases, double floor_eps, double* alpha, int phase_a, int phase_b,
+                       const double* sens_a, const double* sens_b, double target, const double* move,
+                       double damping) {
+  try {
+    topmg::DensityField d(static_cast<int>(ne), 1, nphases, floor_eps);
+    for (long e = 0; e < ne; ++e)
+      for (int i = 0; i < nphases; ++i) d.at(static_cast<int>(e), i) = alpha[e * nphases + i];
+    const std::vector<double> a(sens_a, sens_a + ne), b(sens_b, sens_b + ne), mv(move, move + ne);
+    topmg::oc_update_pair(d, phase_a, phase_b, a, b, target, mv, damping);
+    std::memcpy(alpha, d.values().data(), sizeof(double) * static_cast<std::size_t>(ne) * nphases);
+    return 0;
+  } catch (...) {
+    return map_exception(nullptr, 0, nullptr);
+  }
+}
+
 }  // extern "C"

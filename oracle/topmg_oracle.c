@@ -14,7 +14,7 @@
 #include <string.h>
 #include <time.h>
 
-enum { ST_OK = 0, ST_CONFIG = 1, ST_DIM = 2, ST_DEF = 3, ST_PRECOND = 4 };
+enum { ST_OK = 0, ST_CONFIG = 1, ST_DIM = 2, ST_DEF = 3, ST_PRECOND = 4, ST_MULTIPLIER = 8 };
 
 static double now_s(void) {
   struct timespec ts;
@@ -784,4 +784,86 @@ int orc_filter(int nx, int ny, int np, const double* alpha, int phase, double ra
       out[e] = acc / (alpha[e * np + phase] * ws);
     }
   return ST_OK;
+}
+
+/* std::max / std::min / clamp exactly as <algorithm> evaluates them (mto.cpp:16) */
+static double smax(double a, double b) { return (a < b) ? b : a; }
+static double smin(double a, double b) { return (b < a) ? b : a; }
+static double sclamp(double v, double lo, double hi) { return smin(hi, smax(lo, v)); }
+
+/* One OC exchange between phases a and b (oc_update_pair, mto.cpp:142-227),
+ * in place on the element-major density alpha[e * np + phase]; move is the
+ * per-element move limit. Returns ST_MULTIPLIER when the volume target is
+ * missed after 101 bisection steps. */
+int orc_oc_update_pair(long ne, int np, double floor_eps, double* alpha, int pa, int pb,
+                       const double* sa, const double* sb, double target, const double* move,
+                       double damping) {
+  if (pa == pb) return ST_CONFIG;
+  double* gain = malloc(sizeof(double) * (size_t)ne);
+  double* pair = malloc(sizeof(double) * (size_t)ne);
+  double* lo = malloc(sizeof(double) * (size_t)ne);
+  double* hi = malloc(sizeof(double) * (size_t)ne);
+  double* cand = malloc(sizeof(double) * (size_t)ne);
+  double max_gain = -1e300, max_move = 0.0;
+  for (long e = 0; e < ne; ++e) {
+    gain[e] = sb[e] - sa[e];
+    max_gain = smax(max_gain, gain[e]);
+    max_move = smax(max_move, move[e]);
+    const double a = alpha[e * np + pa];
+    pair[e] = a + alpha[e * np + pb];
+    lo[e] = smax(floor_eps, a - move[e]);
+    hi[e] = smin(pair[e] - floor_eps, a + move[e]);
+  }
+  const double vol_tol = 1e-6;
+  int met = 0;
+  if (max_gain <= 0.0) {
+    double t_lo = -max_move, t_hi = max_move;
+    for (int it = 0; it <= 100; ++it) {
+      const double t = 0.5 * (t_lo + t_hi);
+      double mean = 0.0;
+      for (long e = 0; e < ne; ++e) {
+        cand[e] = sclamp(alpha[e * np + pa] + t, lo[e], hi[e]);
+        mean += cand[e];
+      }
+      mean /= ne;
+      if (fabs(mean - target) <= vol_tol) {
+        met = 1;
+        break;
+      }
+      if (mean > target) t_hi = t;
+      else t_lo = t;
+    }
+  } else {
+    const double floor_gain = 1e-4 * max_gain;
+    double l_lo = 1e-10, l_hi = 1e10;
+    for (int it = 0; it <= 100; ++it) {
+      const double lambda = sqrt(l_lo * l_hi);
+      double mean = 0.0;
+      for (long e = 0; e < ne; ++e) {
+        const double b = smax(floor_gain, gain[e]) / lambda;
+        const double a = alpha[e * np + pa];
+        cand[e] = sclamp(a * pow(b, damping), lo[e], hi[e]);
+        mean += cand[e];
+      }
+      mean /= ne;
+      if (fabs(mean - target) <= vol_tol) {
+        met = 1;
+        break;
+      }
+      if (mean > target) l_lo = lambda;
+      else l_hi = lambda;
+    }
+  }
+  if (met) {
+    for (long e = 0; e < ne; ++e) {
+      alpha[e * np + pa] = cand[e];
+      alpha[e * np + pb] = pair[e] - cand[e];
+    }
+  }
+  free(gain);
+  free(pair);
+  free(lo);
+  free(hi);
+  free(cand);
+  return met ? ST_OK : ST_MULTIPLIER;
 }

@@ -69,6 +69,10 @@ int orc_sensitivities(int nx, int ny, int nphases, const double* alpha,
 /* mto.cpp:87-117 */
 int orc_filter(int nx, int ny, int nphases, const double* alpha, int phase,
                double radius, const double* raw, double* out);
+/* mto.cpp:142-227: in place on alpha[e * nphases + phase]; 8 = MultiplierError */
+int orc_oc_update_pair(long ne, int nphases, double floor_eps, double* alpha, int phase_a,
+                       int phase_b, const double* sens_a, const double* sens_b, double target,
+                       const double* move, double damping);
 
 #ifdef __cplusplus
 }

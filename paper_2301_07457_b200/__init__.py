@@ -32,6 +32,8 @@ from .topmg import (  # noqa: F401
     filter_sensitivities,
     mg_cycle,
     nccl_unique_id,
+    oc_timings,
+    oc_update_pair,
     pcgmg_solve,
     sensitivities,
     slab_partition,

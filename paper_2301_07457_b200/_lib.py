@@ -47,6 +47,9 @@ SIGNATURES = [
     ("tmg_gpu_element_energies", C.c_int, [_H, _D, _D]),
     ("tmg_gpu_sensitivities", C.c_int, [_H, _D, C.c_int, _D, _D, C.c_double, _D]),
     ("tmg_gpu_filter", C.c_int, [_H, C.c_int, _D, C.c_int, C.c_double, _D, _D]),
+    ("tmg_gpu_oc_update_pair", C.c_int,
+     [_H, _D, C.c_int, C.c_double, C.c_int, C.c_int, _D, _D, C.c_double, _D, C.c_double]),
+    ("tmg_gpu_oc_timings", C.c_int, [_H, _D, _I]),
     ("tmg_gpu_apply", C.c_int, [_H, C.c_int, _D, _D]),
     ("tmg_gpu_level_values", C.c_int, [_H, C.c_int, _I, _I, _D]),
     ("tmg_gpu_vcycle", C.c_int, [_H, _D, _D, C.c_int, C.c_int, C.c_int]),

@@ -34,6 +34,7 @@
 #include "tmg_kernels.cuh"
 #include "tmg_march.cuh"
 #include "tmg_smarch.cuh"
+#include "tmg_oc.cuh"
 
 using namespace tmg;
 
@@ -168,6 +169,8 @@ struct Rank {
   long aux_cap = 0;
   double* aux2 = nullptr;
   long aux2_cap = 0;
+  double* ocbuf = nullptr;  // OC exchange scratch (tmg_oc.cuh)
+  long ocbuf_cap = 0;
 
   Level& fine() { return lev[nc]; }
   double2* rbuf(int k) const { return k ? r2 : r; }
@@ -345,6 +348,8 @@ struct tmg_gpu_handle {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t uev[8] = {};
   double last_setup_ms = 0.0, last_pcg_ms = 0.0;
+  double last_oc_ms = 0.0;  // device time of the last OC exchange
+  int last_oc_steps = 0;    // its bisection steps
   std::string err;
   int err_row = -1;
 
@@ -460,7 +465,7 @@ void free_rank(Rank& R) {
                   static_cast<void*>(R.b), static_cast<void*>(R.x0), static_cast<void*>(R.pbuf[0]),
                   static_cast<void*>(R.pbuf[1]), static_cast<void*>(R.partials), static_cast<void*>(R.ticket),
                   static_cast<void*>(R.st), static_cast<void*>(R.scal), static_cast<void*>(R.dense),
-                  static_cast<void*>(R.aux), static_cast<void*>(R.aux2)})
+                  static_cast<void*>(R.aux), static_cast<void*>(R.aux2), static_cast<void*>(R.ocbuf)})
     cudaFree(p);
   if (R.hm) cudaFreeHost(R.hm);
   if (R.scal_host) cudaFreeHost(R.scal_host);
@@ -1698,6 +1703,97 @@ int tmg_gpu_filter(tmg_gpu_handle* h, int nphases, const double* alpha, int phas
     CK(cudaMemcpyAsync(out, d + ne, sizeof(double) * ne, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
   });
+}
+
+int tmg_gpu_oc_update_pair(tmg_gpu_handle* h, double* alpha, int nphases, double floor_eps, int phase_a,
+                           int phase_b, const double* sens_a, const double* sens_b, double target,
+                           const double* move, double damping) {
+  return guarded(h, [&] {
+    need_single(h, "tmg_gpu_oc_update_pair");
+    if (phase_a == phase_b) fail(TMG_ERR_CONFIG, "oc_update_pair: phases must differ");
+    if (phase_a < 0 || phase_b < 0 || phase_a >= nphases || phase_b >= nphases)
+      fail(TMG_ERR_DIMENSION, "oc_update_pair: phase out of range");
+    Rank& R = *h->ranks[0];
+    const long ne = static_cast<long>(h->nx) * h->ny;
+    // cooperative grid: every CTA resident (the bisection crosses grid barriers)
+    static int blocks = 0;
+    if (!blocks) {
+      int dev = 0, sms = 0, per_sm = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_oc_bisect, kOcThreads, 0));
+      if (per_sm < 1) fail(TMG_ERR_CUDA, "k_oc_bisect cannot be resident");
+      blocks = sms * per_sm;
+    }
+    // scratch: density, sens a/b, move, column, gain, lo, hi, maxima, partials,
+    // barrier + flags
+    const long need = ne * nphases + 7 * ne + 2L * blocks + 2L * blocks + 4;
+    double* base = grow(R.ocbuf, R.ocbuf_cap, need);
+    OcArgs a{};
+    a.ne = ne;
+    a.np = nphases;
+    a.pa = phase_a;
+    a.pb = phase_b;
+    a.alpha = base;
+    double* sa = base + ne * nphases;
+    double* sb = sa + ne;
+    double* mv = sb + ne;
+    a.sa = sa;
+    a.sb = sb;
+    a.mv = mv;
+    a.col = mv + ne;
+    a.gain = a.col + ne;
+    a.lo = a.gain + ne;
+    a.hi = a.lo + ne;
+    a.pmax = a.hi + ne;
+    a.part = a.pmax + 2L * blocks;
+    a.bar = reinterpret_cast<unsigned*>(a.part + 2L * blocks);
+    a.met = reinterpret_cast<int*>(a.bar + 2);
+    a.eps = floor_eps;
+    a.target = target;
+    a.damping = damping;
+    CK(cudaMemcpyAsync(a.alpha, alpha, sizeof(double) * ne * nphases, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(sa, sens_a, sizeof(double) * ne, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(sb, sens_b, sizeof(double) * ne, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(mv, move, sizeof(double) * ne, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemsetAsync(a.bar, 0, 4 * sizeof(unsigned), h->stream));
+    CK(cudaEventRecord(h->ev[2], h->stream));
+    k_oc_prep<<<blocks, kOcThreads, 0, h->stream>>>(a);
+    CKL();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(kOcThreads);
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_oc_bisect, a, blocks));
+    CK(cudaEventRecord(h->ev[3], h->stream));
+    h->count(2);
+    int flags[2] = {0, 0};
+    CK(cudaMemcpyAsync(flags, a.met, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]));
+    h->last_oc_ms = ms;
+    h->last_oc_steps = flags[1];
+    if (!flags[0]) {
+      char buf[200];
+      std::snprintf(buf, sizeof buf, "volume target %f for phase %d is unreachable under the current bounds", target,
+                    phase_a + 1);
+      fail(TMG_ERR_MULTIPLIER, buf);
+    }
+    CK(cudaMemcpy(alpha, a.alpha, sizeof(double) * ne * nphases, cudaMemcpyDeviceToHost));
+  });
+}
+
+int tmg_gpu_oc_timings(tmg_gpu_handle* h, double* device_ms, int* steps) {
+  if (!h) return TMG_ERR_DIMENSION;
+  if (device_ms) *device_ms = h->last_oc_ms;
+  if (steps) *steps = h->last_oc_steps;
+  return TMG_OK;
 }
 
 int tmg_gpu_apply(tmg_gpu_handle* h, int level, const double* x, double* y) {

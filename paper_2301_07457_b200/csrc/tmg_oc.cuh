@@ -1,0 +1,175 @@
+// OC exchange between two phases on the device (oc_update_pair,
+// mto.cpp:142-227).
+//
+// The reference bisects for the volume multiplier: up to 101 full element
+// passes, each a clamp(a * (max(floor, gain) / lambda)^damping) (or a clamp of
+// a uniform shift when no element prefers phase a) followed by the mean. Here
+//   k_oc_prep   reads the element-major density once (phases a, b), forms
+//               gain, lo, hi and the phase-a column in SoA scratch and the
+//               per-CTA maxima of gain and of the move limit;
+//   k_oc_bisect runs the whole bisection in one cooperatively launched
+//               persistent grid: per step every CTA reduces its elements,
+//               publishes one partial, crosses a grid barrier and sums the
+//               partials in index order itself, so every CTA takes the same
+//               (deterministic) branch; at the end it writes phases a and b
+//               back into the element-major density.
+// Bytes per element and step: a, gain, lo, hi = 32 (the reference streams
+// the same plus its cand write).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "tmg_kernels.cuh"
+
+namespace tmg {
+
+constexpr int kOcThreads = 256;
+
+struct OcArgs {
+  long ne;
+  int np;            // phases per element (element-major stride)
+  int pa, pb;
+  double* alpha;     // element-major density, device (in/out)
+  const double* sa;  // filtered sensitivities of phases a and b
+  const double* sb;
+  const double* mv;  // per-element move limits
+  double eps;        // density floor
+  double target;
+  double damping;
+  double* col;       // scratch: phase-a column
+  double* gain;
+  double* lo;
+  double* hi;
+  double* pmax;      // per-CTA [max gain, max move] (prep) -> 2 * gridDim
+  double* part;      // per-CTA step partials, 2 * gridDim (double-buffered)
+  unsigned* bar;     // grid barrier [arrivals, generation]
+  int* met;          // out: [0] 1 when the volume target was met, [1] bisection steps
+};
+
+__device__ __forceinline__ double s_max(double a, double b) { return (a < b) ? b : a; }  // std::max
+__device__ __forceinline__ double s_min(double a, double b) { return (b < a) ? b : a; }  // std::min
+__device__ __forceinline__ double s_clamp(double v, double lo, double hi) { return s_min(hi, s_max(lo, v)); }
+
+__global__ void __launch_bounds__(kOcThreads) k_oc_prep(OcArgs a) {
+  double mg = -1e300, mm = 0.0;
+  for (long e = blockIdx.x * static_cast<long>(kOcThreads) + threadIdx.x; e < a.ne;
+       e += static_cast<long>(gridDim.x) * kOcThreads) {
+    const double g = a.sb[e] - a.sa[e];
+    const double m = a.mv[e];
+    const double x = a.alpha[e * a.np + a.pa];
+    const double pair = x + a.alpha[e * a.np + a.pb];
+    mg = s_max(mg, g);
+    mm = s_max(mm, m);
+    a.col[e] = x;
+    a.gain[e] = g;
+    a.lo[e] = s_max(a.eps, x - m);
+    a.hi[e] = s_min(pair - a.eps, x + m);
+  }
+  // block maxima (max is exact in any order)
+  __shared__ double smg[kOcThreads], smm[kOcThreads];
+  smg[threadIdx.x] = mg;
+  smm[threadIdx.x] = mm;
+  __syncthreads();
+  for (int o = kOcThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      smg[threadIdx.x] = s_max(smg[threadIdx.x], smg[threadIdx.x + o]);
+      smm[threadIdx.x] = s_max(smm[threadIdx.x], smm[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    a.pmax[2 * blockIdx.x] = smg[0];
+    a.pmax[2 * blockIdx.x + 1] = smm[0];
+  }
+}
+
+// grid-wide barrier of a cooperatively launched (co-resident) grid
+__device__ __forceinline__ void oc_grid_sync(unsigned* bar, unsigned& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*reinterpret_cast<volatile unsigned*>(bar + 1) == gen) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  ++gen;
+  __syncthreads();
+}
+
+// the candidate of element e for the current step (mto.cpp:176-181, 198-204)
+__device__ __forceinline__ double oc_cand(const OcArgs& a, long e, bool shift, double t, double floor_gain,
+                                          double lambda) {
+  const double x = __ldg(a.col + e);
+  if (shift) return s_clamp(x + t, __ldg(a.lo + e), __ldg(a.hi + e));
+  const double b = s_max(floor_gain, __ldg(a.gain + e)) / lambda;
+  return s_clamp(x * pow(b, a.damping), __ldg(a.lo + e), __ldg(a.hi + e));
+}
+
+__global__ void __launch_bounds__(kOcThreads) k_oc_bisect(OcArgs a, int prep_blocks) {
+  __shared__ double red[kOcThreads / 32];
+  __shared__ double s_mean;
+  __shared__ unsigned s_gen;
+  if (threadIdx.x == 0) s_gen = *reinterpret_cast<volatile unsigned*>(a.bar + 1);
+  // global maxima from the prep partials (identical in every CTA)
+  double max_gain = -1e300, max_move = 0.0;
+  for (int k = 0; k < prep_blocks; ++k) {
+    max_gain = s_max(max_gain, __ldcg(a.pmax + 2 * k));
+    max_move = s_max(max_move, __ldcg(a.pmax + 2 * k + 1));
+  }
+  __syncthreads();
+  unsigned gen = s_gen;
+  const bool shift = !(max_gain > 0.0);  // mto.cpp:170: max_gain <= 0
+  const double floor_gain = 1e-4 * max_gain;
+  const double vol_tol = 1e-6;
+  double t_lo = -max_move, t_hi = max_move, l_lo = 1e-10, l_hi = 1e10;
+  double t = 0.0, lambda = 1.0;
+  bool met = false;
+  const long stride = static_cast<long>(gridDim.x) * kOcThreads;
+  for (int it = 0; it <= 100; ++it) {
+    if (shift) t = 0.5 * (t_lo + t_hi);
+    else lambda = sqrt(l_lo * l_hi);
+    double s = 0.0;
+    for (long e = blockIdx.x * static_cast<long>(kOcThreads) + threadIdx.x; e < a.ne; e += stride)
+      s += oc_cand(a, e, shift, t, floor_gain, lambda);
+    // fixed-shape block tree
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = 0.0;
+      for (int w = 0; w < kOcThreads / 32; ++w) b += red[w];
+      a.part[(it & 1) * gridDim.x + blockIdx.x] = b;
+    }
+    oc_grid_sync(a.bar, gen);
+    if (threadIdx.x == 0) {
+      double sum = 0.0;
+      for (unsigned k = 0; k < gridDim.x; ++k) sum += __ldcg(a.part + (it & 1) * gridDim.x + k);
+      s_mean = sum / static_cast<double>(a.ne);
+    }
+    __syncthreads();
+    const double mean = s_mean;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.met[1] = it + 1;
+    if (fabs(mean - a.target) <= vol_tol) {
+      met = true;
+      break;
+    }
+    if (shift) (mean > a.target ? t_hi : t_lo) = t;
+    else (mean > a.target ? l_lo : l_hi) = lambda;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.met[0] = met ? 1 : 0;
+  if (!met) return;
+  for (long e = blockIdx.x * static_cast<long>(kOcThreads) + threadIdx.x; e < a.ne; e += stride) {
+    const double c = oc_cand(a, e, shift, t, floor_gain, lambda);
+    const double pair = __ldg(a.col + e) + a.alpha[e * a.np + a.pb];
+    a.alpha[e * a.np + a.pa] = c;
+    a.alpha[e * a.np + a.pb] = pair - c;
+  }
+}
+
+}  // namespace tmg

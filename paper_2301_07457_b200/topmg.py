@@ -461,4 +461,33 @@ def filter_sensitivities(ops: MultigridOperators, raw: np.ndarray, alpha: np.nda
     return out
 
 
+def oc_update_pair(ops: MultigridOperators, alpha: np.ndarray, phase_a: int, phase_b: int,
+                   filtered_sens_a: np.ndarray, filtered_sens_b: np.ndarray, target_fraction: float,
+                   move, damping: float, floor_eps: float = 1e-3) -> np.ndarray:
+    """One OC exchange between two phases (oc_update_pair, mto.cpp:142-227)
+    on the device. alpha is the element-major density [ne, nphases] and is
+    updated in place (and returned); move is a scalar or a per-element move
+    limit (both overloads of mto.hpp:66-77). Raises MultiplierError when the
+    volume target cannot be met, ConfigError when the phases coincide."""
+    if not (isinstance(alpha, np.ndarray) and alpha.dtype == np.float64 and alpha.flags.c_contiguous
+            and alpha.ndim == 2):
+        raise DimensionError("oc_update_pair: alpha must be a C-contiguous float64 [ne, nphases] array")
+    ne, nph = alpha.shape
+    sa = np.ascontiguousarray(filtered_sens_a, dtype=np.float64)
+    sb = np.ascontiguousarray(filtered_sens_b, dtype=np.float64)
+    mv = np.ascontiguousarray(np.broadcast_to(np.asarray(move, dtype=np.float64), (ne,)))
+    if ne != ops.grid.element_count() or sa.size != ne or sb.size != ne:
+        raise DimensionError("oc_update_pair: field length does not match grid")
+    ops._check(ops.lib.tmg_gpu_oc_update_pair(ops.h, dptr(alpha), nph, floor_eps, phase_a, phase_b, dptr(sa),
+                                              dptr(sb), target_fraction, dptr(mv), damping))
+    return alpha
+
+
+def oc_timings(ops: MultigridOperators):
+    """(device ms, bisection steps) of the last oc_update_pair."""
+    ms, steps = C.c_double(), C.c_int()
+    ops._check(ops.lib.tmg_gpu_oc_timings(ops.h, C.byref(ms), C.byref(steps)))
+    return ms.value, steps.value
+
+
 __all__ = [n for n in dir() if not n.startswith("_") and n not in ("C", "dataclasses", "np", "dataclass", "field")]

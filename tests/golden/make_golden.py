@@ -4,7 +4,7 @@
 The reference (topopt-mg) ships no golden vectors, so the
 fixtures are produced by running its own code path -- assemble_from_moduli,
 build_multigrid_operators, mg_cycle, pcgmg_solve, compliance,
-element_energies, sensitivities, filter_sensitivities -- through the C-ABI
+element_energies, sensitivities, filter_sensitivities, oc_update_pair -- through the C-ABI
 shim oracle/ref_shim.cpp on small seeded inputs. tests/test_oracle_pin.py
 then pins the committed plain-C oracle to these files bit for bit, so the
 oracle stays pinned even where /root/reference is absent (the GPU box).
@@ -93,6 +93,7 @@ def main():
     if not po.available("ref"):
         raise SystemExit("oracle/_ref/libtopmg_ref.so missing: run `make -C oracle ref`")
     ke = {f"ke_nu{nu}": po.element_stiffness("ref", 1.0, nu) for nu in (0.3, 0.42)}
+    oc = {}
     np.savez_compressed(OUT / "element_stiffness.npz", **ke)
     for name, nx, ny, nc, seed, load, with_x0 in CASES:
         alpha = density(nx, ny, seed)
@@ -127,6 +128,29 @@ def main():
         s.close()
         np.savez_compressed(OUT / f"{name}.npz", **d)
         print(name, "iterations", r["iterations"])
+        oc_cases(name, floored, d["filter_r1.5"], seed, oc)
+    np.savez_compressed(OUT / "oc_pair.npz", **oc)
+
+
+def oc_cases(name, alpha, filt, seed, out):
+    """oc_update_pair (mto.cpp:142-227) on the case's floored density and
+    filtered sensitivities: the multiplicative branch for three phase pairs,
+    the uniform-shift branch (no element prefers phase a) and an unreachable
+    target (MultiplierError, status 8)."""
+    rng = np.random.default_rng(100 + seed)
+    ne = alpha.shape[0]
+    move = rng.uniform(0.02, 0.2, ne)
+    runs = [("mul01", 0, 1, filt[0], filt[1], +0.01), ("mul03", 0, 3, filt[0], filt[3], -0.02),
+            ("mul23", 2, 3, filt[2], filt[3], +0.005),
+            ("shift", 1, 2, filt[2] + np.abs(filt[1]) + 1e-3, filt[2], -0.01),
+            ("unreach", 0, 1, filt[0], filt[1], +0.5)]
+    for tag, pa, pb, sa, sb, dt in runs:
+        target = float(alpha[:, pa].mean() + dt)
+        new, st = po.oc_update_pair("ref", alpha, pa, pb, sa, sb, target, move, 0.5)
+        k = f"{name}_{tag}"
+        out[k + "_alpha"], out[k + "_sa"], out[k + "_sb"], out[k + "_move"] = alpha, sa, sb, move
+        out[k + "_args"] = np.array([pa, pb, target, 0.5, 1e-3])
+        out[k + "_out"], out[k + "_status"] = new, np.array(st)
 
 
 if __name__ == "__main__":

@@ -146,3 +146,40 @@ def test_filter_properties_of_the_reference_tests():
                         ws += w
                         wr += w * raw[jx * ny + jy]
             assert abs(f[ex * ny + ey] * ws - wr) <= 1e-12 * abs(wr)
+
+
+def _oc_runs():
+    d = np.load(GOLDEN / "oc_pair.npz")
+    tags = sorted({k[: -len("_args")] for k in d.files if k.endswith("_args")})
+    return d, tags
+
+
+def test_oc_update_pair_golden_bit_exact():
+    """oc_update_pair (mto.cpp:142-227): both bisection branches and the
+    MultiplierError path, against the reference's own outputs."""
+    d, tags = _oc_runs()
+    assert len(tags) >= 20
+    for t in tags:
+        pa, pb, target, damping, eps = d[t + "_args"]
+        out, st = po.oc_update_pair("orc", d[t + "_alpha"], int(pa), int(pb), d[t + "_sa"], d[t + "_sb"],
+                                    float(target), d[t + "_move"], float(damping), float(eps))
+        assert st == int(d[t + "_status"]), t
+        assert np.array_equal(out, d[t + "_out"]), t
+
+
+def test_oc_update_pair_matches_live_reference():
+    if not po.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(11)
+    for trial in range(8):
+        ne, nph = 300 + 91 * trial, 3 + trial % 2
+        a = rng.uniform(0.05, 1.0, (ne, nph))
+        a /= a.sum(1, keepdims=True)
+        sa, sb = -rng.uniform(0, 2, ne), -rng.uniform(0, 2, ne)
+        if trial == 5:
+            sb = sa - rng.uniform(0.1, 1, ne)  # uniform-shift branch
+        move = rng.uniform(0.01, 0.2, ne) if trial % 3 else np.full(ne, 0.2)
+        target = a[:, 0].mean() + (0.02 if trial % 2 else -0.02)
+        r1, s1 = po.oc_update_pair("ref", a, 0, nph - 1, sa, sb, target, move, 0.3 + 0.1 * trial)
+        r2, s2 = po.oc_update_pair("orc", a, 0, nph - 1, sa, sb, target, move, 0.3 + 0.1 * trial)
+        assert s1 == s2 and np.array_equal(r1, r2)
