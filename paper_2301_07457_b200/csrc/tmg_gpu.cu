@@ -1725,27 +1725,25 @@ int tmg_gpu_oc_update_pair(tmg_gpu_handle* h, double* alpha, int nphases, double
       if (per_sm < 1) fail(TMG_ERR_CUDA, "k_oc_bisect cannot be resident");
       blocks = sms * per_sm;
     }
-    // scratch: density, sens a/b, move, column, gain, lo, hi, maxima, partials,
+    // scratch: the per-element 32-byte records first (aligned at the
+    // allocation base), then density, sens a/b, move, maxima, partials,
     // barrier + flags
-    const long need = ne * nphases + 7 * ne + 2L * blocks + 2L * blocks + 4;
+    const long need = 4 * ne + ne * nphases + 3 * ne + 2L * blocks + 2L * blocks + 4;
     double* base = grow(R.ocbuf, R.ocbuf_cap, need);
     OcArgs a{};
     a.ne = ne;
     a.np = nphases;
     a.pa = phase_a;
     a.pb = phase_b;
-    a.alpha = base;
-    double* sa = base + ne * nphases;
+    a.el = reinterpret_cast<double4*>(base);
+    a.alpha = base + 4 * ne;
+    double* sa = a.alpha + ne * nphases;
     double* sb = sa + ne;
     double* mv = sb + ne;
     a.sa = sa;
     a.sb = sb;
     a.mv = mv;
-    a.col = mv + ne;
-    a.gain = a.col + ne;
-    a.lo = a.gain + ne;
-    a.hi = a.lo + ne;
-    a.pmax = a.hi + ne;
+    a.pmax = mv + ne;
     a.part = a.pmax + 2L * blocks;
     a.bar = reinterpret_cast<unsigned*>(a.part + 2L * blocks);
     a.met = reinterpret_cast<int*>(a.bar + 2);

@@ -5,16 +5,16 @@
 // passes, each a clamp(a * (max(floor, gain) / lambda)^damping) (or a clamp of
 // a uniform shift when no element prefers phase a) followed by the mean. Here
 //   k_oc_prep   reads the element-major density once (phases a, b), forms
-//               gain, lo, hi and the phase-a column in SoA scratch and the
-//               per-CTA maxima of gain and of the move limit;
+//               {a, lo, hi, gain} per element in scratch and the per-CTA
+//               maxima of gain and of the move limit;
 //   k_oc_bisect runs the whole bisection in one cooperatively launched
 //               persistent grid: per step every CTA reduces its elements,
 //               publishes one partial, crosses a grid barrier and sums the
 //               partials in index order itself, so every CTA takes the same
 //               (deterministic) branch; at the end it writes phases a and b
 //               back into the element-major density.
-// Bytes per element and step: a, gain, lo, hi = 32 (the reference streams
-// the same plus its cand write).
+// Bytes per element and step: {a, lo, hi, gain} = 32 in one interleaved
+// stream (the reference streams the same plus its cand write).
 #pragma once
 
 #include <cstdint>
@@ -37,10 +37,7 @@ struct OcArgs {
   double eps;        // density floor
   double target;
   double damping;
-  double* col;       // scratch: phase-a column
-  double* gain;
-  double* lo;
-  double* hi;
+  double4* el;       // scratch per element: {alpha_a, lo, hi, gain} (one 32-byte stream)
   double* pmax;      // per-CTA [max gain, max move] (prep) -> 2 * gridDim
   double* part;      // per-CTA step partials, 2 * gridDim (double-buffered)
   unsigned* bar;     // grid barrier [arrivals, generation]
@@ -61,10 +58,7 @@ __global__ void __launch_bounds__(kOcThreads) k_oc_prep(OcArgs a) {
     const double pair = x + a.alpha[e * a.np + a.pb];
     mg = s_max(mg, g);
     mm = s_max(mm, m);
-    a.col[e] = x;
-    a.gain[e] = g;
-    a.lo[e] = s_max(a.eps, x - m);
-    a.hi[e] = s_min(pair - a.eps, x + m);
+    a.el[e] = make_double4(x, s_max(a.eps, x - m), s_min(pair - a.eps, x + m), g);
   }
   // block maxima (max is exact in any order)
   __shared__ double smg[kOcThreads], smm[kOcThreads];
@@ -102,13 +96,28 @@ __device__ __forceinline__ void oc_grid_sync(unsigned* bar, unsigned& gen) {
   __syncthreads();
 }
 
-// the candidate of element e for the current step (mto.cpp:176-181, 198-204)
-__device__ __forceinline__ double oc_cand(const OcArgs& a, long e, bool shift, double t, double floor_gain,
-                                          double lambda) {
-  const double x = __ldg(a.col + e);
-  if (shift) return s_clamp(x + t, __ldg(a.lo + e), __ldg(a.hi + e));
-  const double b = s_max(floor_gain, __ldg(a.gain + e)) / lambda;
-  return s_clamp(x * pow(b, a.damping), __ldg(a.lo + e), __ldg(a.hi + e));
+// The candidate of element e for the current step (mto.cpp:176-181,
+// 198-204). In the multiplicative branch a.gain holds q = sqrt(max(floor,
+// gain)) for the reference's default damping 0.5 (so the step is a multiply
+// by the uniform 1/sqrt(lambda)), else log(max(floor, gain)) (one exp per
+// element instead of a pow). Both agree with the reference's
+// pow(max(floor, gain) / lambda, damping) to a few ulp.
+struct OcStep {
+  bool shift, half;
+  double t;       // shift branch
+  double scale;   // 1/sqrt(lambda) (half) or log(lambda)
+  double damping;
+};
+__device__ __forceinline__ double oc_cand(const double4 v, const OcStep& s) {
+  // v = {alpha_a, lo, hi, q}
+  if (s.shift) return s_clamp(v.x + s.t, v.y, v.z);
+  const double p = s.half ? v.w * s.scale : exp(s.damping * (v.w - s.scale));
+  return s_clamp(v.x * p, v.y, v.z);
+}
+__device__ __forceinline__ double4 ld_el(const double4* p) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+  const double2 u = __ldg(q), w = __ldg(q + 1);
+  return make_double4(u.x, u.y, w.x, w.y);
 }
 
 __global__ void __launch_bounds__(kOcThreads) k_oc_bisect(OcArgs a, int prep_blocks) {
@@ -124,19 +133,44 @@ __global__ void __launch_bounds__(kOcThreads) k_oc_bisect(OcArgs a, int prep_blo
   }
   __syncthreads();
   unsigned gen = s_gen;
-  const bool shift = !(max_gain > 0.0);  // mto.cpp:170: max_gain <= 0
+  OcStep st{};
+  st.shift = !(max_gain > 0.0);  // mto.cpp:170: max_gain <= 0
+  st.half = a.damping == 0.5;
+  st.damping = a.damping;
   const double floor_gain = 1e-4 * max_gain;
   const double vol_tol = 1e-6;
   double t_lo = -max_move, t_hi = max_move, l_lo = 1e-10, l_hi = 1e10;
-  double t = 0.0, lambda = 1.0;
   bool met = false;
   const long stride = static_cast<long>(gridDim.x) * kOcThreads;
+  if (!st.shift) {
+    // the lambda-independent part of every element's factor, on the elements
+    // this thread owns in every step
+    for (long e = blockIdx.x * static_cast<long>(kOcThreads) + threadIdx.x; e < a.ne; e += stride) {
+      const double g = s_max(floor_gain, a.el[e].w);
+      a.el[e].w = st.half ? sqrt(g) : log(g);
+    }
+  }
   for (int it = 0; it <= 100; ++it) {
-    if (shift) t = 0.5 * (t_lo + t_hi);
-    else lambda = sqrt(l_lo * l_hi);
-    double s = 0.0;
-    for (long e = blockIdx.x * static_cast<long>(kOcThreads) + threadIdx.x; e < a.ne; e += stride)
-      s += oc_cand(a, e, shift, t, floor_gain, lambda);
+    if (st.shift) {
+      st.t = 0.5 * (t_lo + t_hi);
+    } else {
+      const double lambda = sqrt(l_lo * l_hi);
+      st.scale = st.half ? 1.0 / sqrt(lambda) : log(lambda);
+      st.t = lambda;  // kept for the bound update below
+    }
+    // four independent partial sums per thread (fixed order: deterministic)
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    long e = blockIdx.x * static_cast<long>(kOcThreads) + threadIdx.x;
+    for (; e + 3 * stride < a.ne; e += 4 * stride) {
+      const double4 v0 = ld_el(a.el + e), v1 = ld_el(a.el + e + stride), v2 = ld_el(a.el + e + 2 * stride),
+                    v3 = ld_el(a.el + e + 3 * stride);
+      s0 += oc_cand(v0, st);
+      s1 += oc_cand(v1, st);
+      s2 += oc_cand(v2, st);
+      s3 += oc_cand(v3, st);
+    }
+    for (; e < a.ne; e += stride) s0 += oc_cand(ld_el(a.el + e), st);
+    double s = (s0 + s1) + (s2 + s3);
     // fixed-shape block tree
     for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
@@ -159,14 +193,15 @@ __global__ void __launch_bounds__(kOcThreads) k_oc_bisect(OcArgs a, int prep_blo
       met = true;
       break;
     }
-    if (shift) (mean > a.target ? t_hi : t_lo) = t;
-    else (mean > a.target ? l_lo : l_hi) = lambda;
+    if (st.shift) (mean > a.target ? t_hi : t_lo) = st.t;
+    else (mean > a.target ? l_lo : l_hi) = st.t;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) a.met[0] = met ? 1 : 0;
   if (!met) return;
   for (long e = blockIdx.x * static_cast<long>(kOcThreads) + threadIdx.x; e < a.ne; e += stride) {
-    const double c = oc_cand(a, e, shift, t, floor_gain, lambda);
-    const double pair = __ldg(a.col + e) + a.alpha[e * a.np + a.pb];
+    const double4 v = ld_el(a.el + e);
+    const double c = oc_cand(v, st);
+    const double pair = v.x + a.alpha[e * a.np + a.pb];
     a.alpha[e * a.np + a.pa] = c;
     a.alpha[e * a.np + a.pb] = pair - c;
   }
