@@ -12,6 +12,7 @@
 //   compliance(sys.matrix, u)                          -> compliance()
 //   sensitivities(u, density, material, grid)          -> sensitivities(...)
 //   filter_sensitivities(raw, density, i, r, grid)     -> filter_sensitivities(...)
+//   oc_update_pair(density, a, b, fa, fb, V, move, d)  -> oc_update_pair(...)
 // The mesh, supports and hierarchy stay resident on the GPU across outer
 // iterations; only the moduli (or the density) change. See INTEGRATION.md.
 #pragma once
@@ -113,6 +114,30 @@ class PcgmgGpu {
     std::vector<double> out(raw.size());
     check(tmg_gpu_filter(h_, d.num_phases(), d.values().data(), phase, radius, raw.data(), out.data()));
     return out;
+  }
+
+  // oc_update_pair (mto.cpp:142-227), per-element move limits (mto.hpp:73-77)
+  void oc_update_pair(DensityField& d, int phase_a, int phase_b, const std::vector<double>& filtered_sens_a,
+                      const std::vector<double>& filtered_sens_b, double target_fraction,
+                      const std::vector<double>& move, double damping) const {
+    const size_t ne = static_cast<size_t>(d.element_count());
+    if (phase_a == phase_b) throw ConfigError("oc_update_pair: phases must differ");
+    if (filtered_sens_a.size() != ne || filtered_sens_b.size() != ne || move.size() != ne)
+      throw DimensionError("oc_update_pair: field length does not match grid");
+    std::vector<double> v = d.values();
+    check(tmg_gpu_oc_update_pair(h_, v.data(), d.num_phases(), d.floor_eps(), phase_a, phase_b,
+                                 filtered_sens_a.data(), filtered_sens_b.data(), target_fraction, move.data(),
+                                 damping));
+    for (size_t e = 0; e < ne; ++e)
+      for (int i = 0; i < d.num_phases(); ++i)
+        d.at(static_cast<int>(e), i) = v[e * static_cast<size_t>(d.num_phases()) + static_cast<size_t>(i)];
+  }
+  // the scalar move-limit overload (mto.hpp:66-69)
+  void oc_update_pair(DensityField& d, int phase_a, int phase_b, const std::vector<double>& filtered_sens_a,
+                      const std::vector<double>& filtered_sens_b, double target_fraction, double move,
+                      double damping) const {
+    oc_update_pair(d, phase_a, phase_b, filtered_sens_a, filtered_sens_b, target_fraction,
+                   std::vector<double>(static_cast<size_t>(d.element_count()), move), damping);
   }
 
   tmg_gpu_handle* handle() const { return h_; }

@@ -10,6 +10,7 @@
 //
 // Prints one line per design:  k iters_ref iters_gpu relerr_u relerr_C
 //                              max_relerr_sens max_relerr_filtered
+//                              max_abs_density_diff_after_oc_sweep
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -99,16 +100,30 @@ int main(int argc, char** argv) {
     const double c_gpu = dev.compliance();
     const auto s_gpu = dev.sensitivities(d, mat);
     double es = 0.0, ef = 0.0;
+    std::vector<std::vector<double>> filt(static_cast<size_t>(mat.num_phases()));
     for (int i = 0; i < mat.num_phases(); ++i) {
       es = std::max(es, maxrel(s_gpu[i], s_ref[i]));
       const auto f_ref = filter_sensitivities(s_ref[i], d, i, cfg.filter_radius, prob.grid);
       const auto f_gpu = dev.filter_sensitivities(s_gpu[i], d, i, cfg.filter_radius);
       ef = std::max(ef, maxrel(f_gpu, f_ref));
+      filt[static_cast<size_t>(i)] = f_ref;
     }
+    // the OC pair sweep of mto.cpp:312-323 (one sweep per pair, the default
+    // inner_sweeps) from the same filtered sensitivities: reference vs GPU
+    DensityField d_ref = d, d_gpu = d;
+    const std::vector<double> move(static_cast<size_t>(d.element_count()), cfg.move_limit);
+    for (int a = 0; a < mat.num_phases() - 1; ++a)
+      for (int b = a + 1; b < mat.num_phases(); ++b) {
+        oc_update_pair(d_ref, a, b, filt[static_cast<size_t>(a)], filt[static_cast<size_t>(b)],
+                       cfg.volume_fractions[static_cast<size_t>(a)], move, cfg.oc_damping);
+        dev.oc_update_pair(d_gpu, a, b, filt[static_cast<size_t>(a)], filt[static_cast<size_t>(b)],
+                           cfg.volume_fractions[static_cast<size_t>(a)], move, cfg.oc_damping);
+      }
+    const double eoc = DensityField::max_change(d_gpu, d_ref);
     const double eu = rel(got.solution, ref.solution), ec = std::abs(c_gpu - c_ref) / std::abs(c_ref);
-    std::printf("%d %d %d %.3e %.3e %.3e %.3e\n", k, ref.iterations, got.iterations, eu, ec, es, ef);
+    std::printf("%d %d %d %.3e %.3e %.3e %.3e %.3e\n", k, ref.iterations, got.iterations, eu, ec, es, ef, eoc);
     if (!(eu <= 1e-8 && ec <= 1e-9 && std::abs(ref.iterations - got.iterations) <= 2 && es <= 1e-8 &&
-          ef <= 1e-8))
+          ef <= 1e-8 && eoc <= 1e-12))
       ++bad;
   }
   return bad;

@@ -1,5 +1,6 @@
-"""C++ drop-in check: the reference optimizer's designs solved by the
-reference and by include/topmg_gpu.hpp (tests/cpp/dropin_check.cpp)."""
+"""C++ drop-in check: the reference optimizer's designs solved, and their OC
+pair sweep applied, by the reference and by include/topmg_gpu.hpp
+(tests/cpp/dropin_check.cpp)."""
 import pathlib
 import subprocess
 
@@ -15,8 +16,10 @@ def test_cpp_dropin_matches_reference_on_optimizer_designs():
     p = subprocess.run([str(BIN), "64", "6"], capture_output=True, text=True, timeout=600)
     lines = [l.split() for l in p.stdout.strip().splitlines()]
     assert len(lines) == 6, p.stdout + p.stderr
-    for k, it_ref, it_gpu, eu, ec, es, ef in lines:
+    for k, it_ref, it_gpu, eu, ec, es, ef, eoc in lines:
         assert abs(int(it_ref) - int(it_gpu)) <= 2
         assert float(eu) <= 1e-8 and float(ec) <= 1e-9
         assert float(es) <= 1e-8 and float(ef) <= 1e-8
+        # the OC pair sweep (mto.cpp:312-323) through topmg_gpu.hpp
+        assert float(eoc) <= 1e-12
     assert p.returncode == 0, p.stdout + p.stderr
