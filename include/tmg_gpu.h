@@ -177,6 +177,35 @@ int tmg_gpu_filter(tmg_gpu_handle* h, int nphases, const double* alpha, int phas
 int tmg_gpu_oc_update_pair(tmg_gpu_handle* h, double* alpha, int nphases, double floor_eps,
                            int phase_a, int phase_b, const double* sens_a, const double* sens_b,
                            double target, const double* move, double damping);
+/* OptimConfig (mto.hpp:12-27) with Method::pcgmg, flattened; Poisson's ratio
+ * is the handle's (tmg_gpu_set_problem). */
+typedef struct {
+  int nphases;
+  const double* phase_moduli;     /* MaterialModel::phase_moduli [nphases] */
+  double penalty;                 /* MaterialModel::penalty */
+  const double* volume_fractions; /* [nphases] */
+  double filter_radius, filter_tol, tol;
+  int inner_sweeps;
+  double move_limit, oc_damping;
+  int warm_start, max_outer;
+  double density_floor;
+  double solver_tol;              /* SolverConfig */
+  int solver_max_iter, gamma, pre_sweeps, post_sweeps;
+  double omega;
+} tmg_optim_config;
+
+/* The whole optimizer, optimize() with Method::pcgmg (mto.cpp:229-354), with
+ * every per-iteration step on the device: effective moduli + Galerkin
+ * setup, the warm-startable solve, compliance, sensitivities, the filter,
+ * the OC pair sweeps, the move-limit adaptation and the max-change test.
+ * rhs: the load vector (fixed dofs zero). Outputs mirror OptimReport: the
+ * final element-major density [ne * nphases] and per outer iteration the
+ * compliance, max density change, solver iterations and seconds (arrays of
+ * max_outer entries). Single-rank handles. */
+int tmg_gpu_optimize(tmg_gpu_handle* h, const tmg_optim_config* cfg, const double* rhs,
+                     double* density_out, double* compliance_hist, double* change_hist,
+                     int* iters_hist, double* seconds_hist, int* outer_iterations,
+                     long* total_solver_iterations, int* converged, double* seconds);
 /* Device time (ms) and bisection steps of the last tmg_gpu_oc_update_pair. */
 int tmg_gpu_oc_timings(tmg_gpu_handle* h, double* device_ms, int* steps);
 

@@ -233,3 +233,37 @@ def oc_update_pair(kind, alpha, phase_a, phase_b, sens_a, sens_b, target, move, 
     f.argtypes = [C.c_long, C.c_int, C.c_double, _D, C.c_int, C.c_int, _D, _D, C.c_double, _D, C.c_double]
     st = f(ne, nph, floor_eps, _d(a), phase_a, phase_b, _d(sa), _d(sb), target, _d(mv), damping)
     return a, st
+
+
+def optimize(kind, nx, ny, fixed, loads, phase_moduli, penalty, nu, fractions, filter_radius=1.5,
+             filter_tol=0.05, tol=1e-3, inner_sweeps=1, move_limit=0.2, oc_damping=0.5, warm_start=False,
+             max_outer=10, density_floor=1e-3, num_coarsenings=2, omega=0.6, solver_tol=1e-8,
+             solver_max_iter=2000, gamma=1, pre=2, post=2):
+    """optimize() with Method::pcgmg (mto.cpp:229-354). Returns a dict with the
+    OptimReport fields; raises OracleError on a reference exception."""
+    np_ = len(phase_moduli)
+    fx = np.ascontiguousarray(fixed, dtype=np.int32)
+    ld = np.ascontiguousarray([l[0] for l in loads], dtype=np.int32)
+    lv = np.ascontiguousarray([l[1] for l in loads], dtype=np.float64)
+    pm = np.ascontiguousarray(phase_moduli, dtype=np.float64)
+    fr = np.ascontiguousarray(fractions, dtype=np.float64)
+    dens = np.empty(nx * ny * np_)
+    ch, dh = np.zeros(max_outer), np.zeros(max_outer)
+    ih = np.zeros(max_outer, dtype=np.int32)
+    oi, cv = C.c_int(), C.c_int()
+    ti = C.c_long()
+    err = C.create_string_buffer(256)
+    f = getattr(lib(kind), kind + "_optimize")
+    f.restype = C.c_int
+    st = f(nx, ny, np_, _d(pm), C.c_double(penalty), C.c_double(nu), fx.ctypes.data_as(_I), len(fx),
+           ld.ctypes.data_as(_I), _d(lv), len(lv), _d(fr), C.c_double(filter_radius), C.c_double(filter_tol),
+           C.c_double(tol), inner_sweeps, C.c_double(move_limit), C.c_double(oc_damping), int(warm_start),
+           max_outer, C.c_double(density_floor), num_coarsenings, C.c_double(omega), C.c_double(solver_tol),
+           solver_max_iter, gamma, pre, post, _d(dens), _d(ch), _d(dh), ih.ctypes.data_as(_I), C.byref(oi),
+           C.byref(ti), C.byref(cv), err, 256)
+    if st:
+        raise OracleError(st, err.value.decode())
+    k = oi.value
+    return dict(density=dens.reshape(nx * ny, np_), compliance_history=ch[:k], change_history=dh[:k],
+                solver_iteration_history=ih[:k], outer_iterations=k, total_solver_iterations=ti.value,
+                converged=bool(cv.value))

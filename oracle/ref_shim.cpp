@@ -329,4 +329,54 @@ int ref_oc_update_pair(long ne, int nphases, double floor_eps, double* alpha, in
   }
 }
 
+int ref_optimize(int nx, int ny, int np, const double* pm, double penalty, double nu, const int* fixed, int n_fixed,
+                 const int* load_dofs, const double* load_vals, int n_loads, const double* fractions,
+                 double filter_radius, double filter_tol, double tol, int inner_sweeps, double move_limit,
+                 double oc_damping, int warm_start, int max_outer, double density_floor, int num_coarsenings,
+                 double omega, double solver_tol, int solver_max_iter, int gamma, int pre, int post,
+                 double* density, double* compliance_hist, double* change_hist, int* iters_hist,
+                 int* outer_iterations, long* total_iters, int* converged, char* err, int errlen) {
+  try {
+    topmg::Problem prob;
+    prob.grid = topmg::GridLevel{nx, ny, 2, 0};
+    prob.bc.fixed_dofs.assign(fixed, fixed + n_fixed);
+    for (int k = 0; k < n_loads; ++k) prob.bc.point_loads.emplace_back(load_dofs[k], load_vals[k]);
+    prob.material.phase_moduli.assign(pm, pm + np);
+    prob.material.poisson_ratio = nu;
+    prob.material.penalty = penalty;
+    topmg::OptimConfig cfg;
+    cfg.volume_fractions.assign(fractions, fractions + np);
+    cfg.filter_radius = filter_radius;
+    cfg.filter_tol = filter_tol;
+    cfg.tol = tol;
+    cfg.inner_sweeps = inner_sweeps;
+    cfg.move_limit = move_limit;
+    cfg.oc_damping = oc_damping;
+    cfg.warm_start = warm_start != 0;
+    cfg.max_outer = max_outer;
+    cfg.density_floor = density_floor;
+    cfg.solver.method = topmg::Method::pcgmg;
+    cfg.solver.num_coarsenings = num_coarsenings;
+    cfg.solver.omega = omega;
+    cfg.solver.tol = solver_tol;
+    cfg.solver.max_iter = solver_max_iter;
+    cfg.solver.gamma = gamma;
+    cfg.solver.pre_sweeps = pre;
+    cfg.solver.post_sweeps = post;
+    const topmg::OptimReport r = topmg::optimize(prob, cfg);
+    std::memcpy(density, r.density.values().data(), sizeof(double) * r.density.values().size());
+    for (size_t k = 0; k < r.compliance_history.size(); ++k) {
+      compliance_hist[k] = r.compliance_history[k];
+      change_hist[k] = r.change_history[k];
+      iters_hist[k] = r.solver_iteration_history[k];
+    }
+    *outer_iterations = r.outer_iterations;
+    *total_iters = r.total_solver_iterations;
+    *converged = r.converged ? 1 : 0;
+    return 0;
+  } catch (...) {
+    return map_exception(err, errlen, nullptr);
+  }
+}
+
 }  // extern "C"

@@ -867,3 +867,117 @@ int orc_oc_update_pair(long ne, int np, double floor_eps, double* alpha, int pa,
   free(cand);
   return met ? ST_OK : ST_MULTIPLIER;
 }
+
+/* max |a - b| over all entries (DensityField::max_change, density.cpp:60-66) */
+static double max_change(const double* a, const double* b, long n) {
+  double w = 0.0;
+  for (long i = 0; i < n; ++i) w = smax(w, fabs(a[i] - b[i]));
+  return w;
+}
+
+/* optimize() with Method::pcgmg (mto.cpp:229-354): uniform start, per outer
+ * iteration assemble (effective moduli + system), build_multigrid_operators,
+ * pcgmg_solve (warm start optional), compliance, sensitivities, filtered
+ * sensitivities, the OC pair sweeps, the per-element move-limit adaptation
+ * and the max-change convergence test. Histories hold up to max_outer
+ * entries. */
+int orc_optimize(int nx, int ny, int np, const double* pm, double penalty, double nu, const int* fixed,
+                 int n_fixed, const int* load_dofs, const double* load_vals, int n_loads, const double* fractions,
+                 double filter_radius, double filter_tol, double tol, int inner_sweeps, double move_limit,
+                 double oc_damping, int warm_start, int max_outer, double density_floor, int num_coarsenings,
+                 double omega, double solver_tol, int solver_max_iter, int gamma, int pre, int post,
+                 double* density, double* compliance_hist, double* change_hist, int* iters_hist,
+                 int* outer_iterations, long* total_iters, int* converged, char* err, int errlen) {
+  const long ne = (long)nx * ny, nv = ne * np, n = 2L * (nx + 1) * (ny + 1);
+  int st = ST_OK;
+  for (long e = 0; e < ne; ++e)
+    for (int i = 0; i < np; ++i) density[e * np + i] = fractions[i];  /* DensityField::uniform */
+  double* move = malloc(sizeof(double) * (size_t)ne);
+  double* last = calloc((size_t)nv, sizeof(double));
+  double* before = malloc(sizeof(double) * (size_t)nv);
+  double* pre_sweep = malloc(sizeof(double) * (size_t)nv);
+  double* E = malloc(sizeof(double) * (size_t)ne);
+  double* u = malloc(sizeof(double) * (size_t)n);
+  double* x = malloc(sizeof(double) * (size_t)n);
+  double* rhs = malloc(sizeof(double) * (size_t)n);
+  double* hist = malloc(sizeof(double) * (size_t)(solver_max_iter + 1));
+  double* raw = malloc(sizeof(double) * (size_t)nv);
+  double* filt = malloc(sizeof(double) * (size_t)nv);
+  for (long e = 0; e < ne; ++e) move[e] = move_limit;
+  int have_u = 0;
+  *outer_iterations = 0;
+  *total_iters = 0;
+  *converged = 0;
+  for (int outer = 1; outer <= max_outer; ++outer) {
+    orc_effective_moduli(nx, ny, np, density, pm, penalty, E);
+    void* s = orc_system_create(nx, ny, E, nu, fixed, n_fixed, load_dofs, load_vals, n_loads, err, errlen, &st);
+    if (st) break;
+    int row = -1;
+    st = orc_system_build_mg(s, num_coarsenings, omega, err, errlen, &row);
+    if (!st) {
+      orc_system_rhs(s, rhs);
+      int it = 0, cv = 0, hl = 0;
+      double fr = 0.0;
+      st = orc_system_solve(s, rhs, (warm_start && have_u) ? u : NULL, solver_tol, solver_max_iter, gamma, pre,
+                            post, x, &it, &fr, &cv, hist, &hl, err, errlen);
+      if (!st) {
+        memcpy(u, x, sizeof(double) * (size_t)n);
+        have_u = 1;
+        compliance_hist[outer - 1] = orc_system_compliance(s, u);
+        iters_hist[outer - 1] = it;
+        *total_iters += it;
+      }
+    }
+    orc_system_destroy(s);
+    if (st) break;
+    orc_sensitivities(nx, ny, np, density, pm, penalty, nu, u, raw);
+    for (int i = 0; i < np; ++i) orc_filter(nx, ny, np, density, i, filter_radius, raw + i * ne, filt + i * ne);
+    memcpy(before, density, sizeof(double) * (size_t)nv);
+    for (int a = 0; a < np - 1 && !st; ++a)
+      for (int b = a + 1; b < np && !st; ++b)
+        for (int sweep = 0; sweep < inner_sweeps; ++sweep) {
+          memcpy(pre_sweep, density, sizeof(double) * (size_t)nv);
+          st = orc_oc_update_pair(ne, np, density_floor, density, a, b, filt + a * ne, filt + b * ne, fractions[a],
+                                  move, oc_damping);
+          if (st) {
+            if (err && errlen > 0)
+              snprintf(err, (size_t)errlen, "volume target %f for phase %d is unreachable under the current bounds",
+                       fractions[a], a + 1);
+            break;
+          }
+          if (max_change(density, pre_sweep, nv) <= filter_tol) break;
+        }
+    if (st) break;
+    for (long e = 0; e < ne; ++e) {
+      int flipped = 0, moved = 0;
+      for (int i = 0; i < np; ++i) {
+        const double delta = density[e * np + i] - before[e * np + i];
+        double* l = &last[e * np + i];
+        if (fabs(delta) > 1e-12) moved = 1;
+        if (delta * *l < -1e-12) flipped = 1;
+        *l = delta;
+      }
+      if (flipped) move[e] = smax(1e-4, 0.5 * move[e]);
+      else if (moved) move[e] = smin(move_limit, 1.05 * move[e]);
+    }
+    const double change = max_change(density, before, nv);
+    change_hist[outer - 1] = change;
+    *outer_iterations = outer;
+    if (change <= tol) {
+      *converged = 1;
+      break;
+    }
+  }
+  free(move);
+  free(last);
+  free(before);
+  free(pre_sweep);
+  free(E);
+  free(u);
+  free(x);
+  free(rhs);
+  free(hist);
+  free(raw);
+  free(filt);
+  return st;
+}

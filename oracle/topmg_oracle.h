@@ -73,6 +73,16 @@ int orc_filter(int nx, int ny, int nphases, const double* alpha, int phase,
 int orc_oc_update_pair(long ne, int nphases, double floor_eps, double* alpha, int phase_a,
                        int phase_b, const double* sens_a, const double* sens_b, double target,
                        const double* move, double damping);
+/* optimize() with Method::pcgmg (mto.cpp:229-354); density [ne * np] out,
+ * histories of up to max_outer entries */
+int orc_optimize(int nx, int ny, int np, const double* phase_moduli, double penalty, double nu,
+                 const int* fixed, int n_fixed, const int* load_dofs, const double* load_vals,
+                 int n_loads, const double* fractions, double filter_radius, double filter_tol,
+                 double tol, int inner_sweeps, double move_limit, double oc_damping, int warm_start,
+                 int max_outer, double density_floor, int num_coarsenings, double omega,
+                 double solver_tol, int solver_max_iter, int gamma, int pre, int post,
+                 double* density, double* compliance_hist, double* change_hist, int* iters_hist,
+                 int* outer_iterations, long* total_iters, int* converged, char* err, int errlen);
 
 #ifdef __cplusplus
 }

@@ -32,7 +32,10 @@ from .topmg import (  # noqa: F401
     filter_sensitivities,
     mg_cycle,
     nccl_unique_id,
+    OptimConfig,
+    OptimReport,
     oc_timings,
+    optimize,
     oc_update_pair,
     pcgmg_solve,
     sensitivities,

@@ -20,6 +20,16 @@ _I = C.POINTER(C.c_int)
 _H = C.c_void_p
 
 # (name, restype, argtypes) for every symbol include/tmg_gpu.h declares
+class OptimConfigC(C.Structure):
+    """tmg_optim_config (include/tmg_gpu.h): OptimConfig + SolverConfig flattened."""
+    _fields_ = [("nphases", C.c_int), ("phase_moduli", _D), ("penalty", C.c_double),
+                ("volume_fractions", _D), ("filter_radius", C.c_double), ("filter_tol", C.c_double),
+                ("tol", C.c_double), ("inner_sweeps", C.c_int), ("move_limit", C.c_double),
+                ("oc_damping", C.c_double), ("warm_start", C.c_int), ("max_outer", C.c_int),
+                ("density_floor", C.c_double), ("solver_tol", C.c_double), ("solver_max_iter", C.c_int),
+                ("gamma", C.c_int), ("pre_sweeps", C.c_int), ("post_sweeps", C.c_int), ("omega", C.c_double)]
+
+
 SIGNATURES = [
     ("tmg_gpu_create", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_H)]),
     ("tmg_gpu_destroy", None, [_H]),
@@ -50,6 +60,8 @@ SIGNATURES = [
     ("tmg_gpu_oc_update_pair", C.c_int,
      [_H, _D, C.c_int, C.c_double, C.c_int, C.c_int, _D, _D, C.c_double, _D, C.c_double]),
     ("tmg_gpu_oc_timings", C.c_int, [_H, _D, _I]),
+    ("tmg_gpu_optimize", C.c_int, [_H, C.POINTER(OptimConfigC), _D, _D, _D, _D, _I, _D, _I,
+                                   C.POINTER(C.c_long), _I, _D]),
     ("tmg_gpu_apply", C.c_int, [_H, C.c_int, _D, _D]),
     ("tmg_gpu_level_values", C.c_int, [_H, C.c_int, _I, _I, _D]),
     ("tmg_gpu_vcycle", C.c_int, [_H, _D, _D, C.c_int, C.c_int, C.c_int]),

@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1705,6 +1706,88 @@ int tmg_gpu_filter(tmg_gpu_handle* h, int nphases, const double* alpha, int phas
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// Scratch of one OC exchange on rank 0: the per-element 32-byte records
+// first (aligned at the allocation base), then maxima, partials, barrier and
+// flags. Grown on demand; `extra` doubles after it are the caller's.
+double* oc_scratch(Rank& R, long ne, long extra, int blocks) {
+  return grow(R.ocbuf, R.ocbuf_cap, 4 * ne + 4L * blocks + 4 + extra);
+}
+
+int oc_blocks() {
+  static int blocks = 0;
+  if (!blocks) {
+    int dev = 0, sms = 0, per_sm = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_oc_bisect, kOcThreads, 0));
+    if (per_sm < 1) fail(TMG_ERR_CUDA, "k_oc_bisect cannot be resident");
+    blocks = sms * per_sm;
+  }
+  return blocks;
+}
+
+// One OC exchange on device data (oc_update_pair, mto.cpp:142-227): alpha
+// element-major, sens a/b and move per element, all on rank 0's device.
+// Throws TMG_ERR_MULTIPLIER (alpha unchanged) like the reference.
+void oc_pair_device(H* h, Rank& R, double* scratch, double* alpha, long ne, int np, double eps, int pa, int pb,
+                    const double* sa, const double* sb, double target, const double* mv, double damping) {
+  const int blocks = oc_blocks();
+  OcArgs a{};
+  a.ne = ne;
+  a.np = np;
+  a.pa = pa;
+  a.pb = pb;
+  a.el = reinterpret_cast<double4*>(scratch);
+  a.pmax = scratch + 4 * ne;
+  a.part = a.pmax + 2L * blocks;
+  a.bar = reinterpret_cast<unsigned*>(a.part + 2L * blocks);
+  a.met = reinterpret_cast<int*>(a.bar + 2);
+  a.alpha = alpha;
+  a.sa = sa;
+  a.sb = sb;
+  a.mv = mv;
+  a.eps = eps;
+  a.target = target;
+  a.damping = damping;
+  CK(cudaMemsetAsync(a.bar, 0, 4 * sizeof(unsigned), h->stream));
+  CK(cudaEventRecord(h->ev[2], h->stream));
+  k_oc_prep<<<blocks, kOcThreads, 0, h->stream>>>(a);
+  CKL();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kOcThreads);
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: the bisection crosses grid barriers
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_oc_bisect, a, blocks));
+  CK(cudaEventRecord(h->ev[3], h->stream));
+  h->count(2);
+  int* flags = reinterpret_cast<int*>(R.scal_host);
+  CK(cudaMemcpyAsync(flags, a.met, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]));
+  h->last_oc_ms = ms;
+  h->last_oc_steps = flags[1];
+  if (!flags[0]) {
+    char buf[200];
+    std::snprintf(buf, sizeof buf, "volume target %f for phase %d is unreachable under the current bounds", target,
+                  pa + 1);
+    fail(TMG_ERR_MULTIPLIER, buf);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
 int tmg_gpu_oc_update_pair(tmg_gpu_handle* h, double* alpha, int nphases, double floor_eps, int phase_a,
                            int phase_b, const double* sens_a, const double* sens_b, double target,
                            const double* move, double damping) {
@@ -1715,75 +1798,181 @@ int tmg_gpu_oc_update_pair(tmg_gpu_handle* h, double* alpha, int nphases, double
       fail(TMG_ERR_DIMENSION, "oc_update_pair: phase out of range");
     Rank& R = *h->ranks[0];
     const long ne = static_cast<long>(h->nx) * h->ny;
-    // cooperative grid: every CTA resident (the bisection crosses grid barriers)
-    static int blocks = 0;
-    if (!blocks) {
-      int dev = 0, sms = 0, per_sm = 0;
-      CK(cudaGetDevice(&dev));
-      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_oc_bisect, kOcThreads, 0));
-      if (per_sm < 1) fail(TMG_ERR_CUDA, "k_oc_bisect cannot be resident");
-      blocks = sms * per_sm;
-    }
-    // scratch: the per-element 32-byte records first (aligned at the
-    // allocation base), then density, sens a/b, move, maxima, partials,
-    // barrier + flags
-    const long need = 4 * ne + ne * nphases + 3 * ne + 2L * blocks + 2L * blocks + 4;
-    double* base = grow(R.ocbuf, R.ocbuf_cap, need);
-    OcArgs a{};
-    a.ne = ne;
-    a.np = nphases;
-    a.pa = phase_a;
-    a.pb = phase_b;
-    a.el = reinterpret_cast<double4*>(base);
-    a.alpha = base + 4 * ne;
-    double* sa = a.alpha + ne * nphases;
+    // scratch, then the uploaded density, sens a/b and move
+    const int blocks = oc_blocks();
+    double* scratch = oc_scratch(R, ne, ne * nphases + 3 * ne, blocks);
+    double* d_alpha = scratch + 4 * ne + 4L * blocks + 4;
+    double* sa = d_alpha + ne * nphases;
     double* sb = sa + ne;
     double* mv = sb + ne;
-    a.sa = sa;
-    a.sb = sb;
-    a.mv = mv;
-    a.pmax = mv + ne;
-    a.part = a.pmax + 2L * blocks;
-    a.bar = reinterpret_cast<unsigned*>(a.part + 2L * blocks);
-    a.met = reinterpret_cast<int*>(a.bar + 2);
-    a.eps = floor_eps;
-    a.target = target;
-    a.damping = damping;
-    CK(cudaMemcpyAsync(a.alpha, alpha, sizeof(double) * ne * nphases, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(d_alpha, alpha, sizeof(double) * ne * nphases, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(sa, sens_a, sizeof(double) * ne, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(sb, sens_b, sizeof(double) * ne, cudaMemcpyHostToDevice, h->stream));
     CK(cudaMemcpyAsync(mv, move, sizeof(double) * ne, cudaMemcpyHostToDevice, h->stream));
-    CK(cudaMemsetAsync(a.bar, 0, 4 * sizeof(unsigned), h->stream));
-    CK(cudaEventRecord(h->ev[2], h->stream));
-    k_oc_prep<<<blocks, kOcThreads, 0, h->stream>>>(a);
-    CKL();
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(blocks);
-    cfg.blockDim = dim3(kOcThreads);
-    cfg.stream = h->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, k_oc_bisect, a, blocks));
-    CK(cudaEventRecord(h->ev[3], h->stream));
-    h->count(2);
-    int flags[2] = {0, 0};
-    CK(cudaMemcpyAsync(flags, a.met, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]));
-    h->last_oc_ms = ms;
-    h->last_oc_steps = flags[1];
-    if (!flags[0]) {
-      char buf[200];
-      std::snprintf(buf, sizeof buf, "volume target %f for phase %d is unreachable under the current bounds", target,
-                    phase_a + 1);
-      fail(TMG_ERR_MULTIPLIER, buf);
+    oc_pair_device(h, R, scratch, d_alpha, ne, nphases, floor_eps, phase_a, phase_b, sa, sb, target, mv, damping);
+    CK(cudaMemcpy(alpha, d_alpha, sizeof(double) * ne * nphases, cudaMemcpyDeviceToHost));
+  });
+}
+
+int tmg_gpu_optimize(tmg_gpu_handle* h, const tmg_optim_config* c, const double* rhs, double* density_out,
+                     double* compliance_hist, double* change_hist, int* iters_hist, double* seconds_hist,
+                     int* outer_iterations, long* total_solver_iterations, int* converged, double* seconds) {
+  return guarded(h, [&] {
+    using clk = std::chrono::steady_clock;
+    const auto t_start = clk::now();
+    need_single(h, "tmg_gpu_optimize");
+    if (!h->have_problem) fail(TMG_ERR_DIMENSION, "tmg_gpu_set_problem must precede tmg_gpu_optimize");
+    // OptimConfig::validate (mto.cpp:20-50), MaterialModel::validate
+    // (density.cpp:10-27), SolverConfig::validate (solvers.cpp:70-87)
+    const int np = c->nphases;
+    if (np < 2) fail(TMG_ERR_CONFIG, "need at least two phases (one material plus void)");
+    double sum = 0.0;
+    for (int i = 0; i < np; ++i) {
+      const double v = c->volume_fractions[i];
+      if (!(v > 0.0 && v < 1.0))
+        fail(TMG_ERR_CONFIG, "volume_fractions entries must lie in (0, 1), got " + std::to_string(v));
+      sum += v;
     }
-    CK(cudaMemcpy(alpha, a.alpha, sizeof(double) * ne * nphases, cudaMemcpyDeviceToHost));
+    if (std::abs(sum - 1.0) > 1e-12) fail(TMG_ERR_CONFIG, "volume_fractions must sum to 1, got " + std::to_string(sum));
+    if (c->filter_radius < 0.0) fail(TMG_ERR_CONFIG, "filter_radius must be >= 0");
+    if (!(c->filter_tol > 0.0)) fail(TMG_ERR_CONFIG, "filter_tol must be positive");
+    if (!(c->tol > 0.0)) fail(TMG_ERR_CONFIG, "tol must be positive");
+    if (c->inner_sweeps < 1) fail(TMG_ERR_CONFIG, "inner_sweeps must be >= 1");
+    if (!(c->move_limit > 0.0 && c->move_limit <= 1.0)) fail(TMG_ERR_CONFIG, "move_limit must lie in (0, 1]");
+    if (!(c->oc_damping > 0.0 && c->oc_damping <= 1.0)) fail(TMG_ERR_CONFIG, "oc_damping must lie in (0, 1]");
+    if (c->max_outer < 1) fail(TMG_ERR_CONFIG, "max_outer must be >= 1");
+    if (!(c->density_floor > 0.0 && c->density_floor < 0.5))
+      fail(TMG_ERR_CONFIG, "density_floor must lie in (0, 0.5)");
+    if (!(c->solver_tol > 0.0)) fail(TMG_ERR_CONFIG, "solver tol must be positive");
+    if (c->solver_max_iter < 1) fail(TMG_ERR_CONFIG, "max_iter must be >= 1");
+    if (!(c->omega > 0.0 && c->omega <= 1.0))
+      fail(TMG_ERR_CONFIG, "omega must lie in (0, 1], got " + std::to_string(c->omega));
+    if (c->gamma != 1 && c->gamma != 2) fail(TMG_ERR_CONFIG, "gamma must be 1 (V-cycle) or 2 (W-cycle)");
+    if (c->pre_sweeps < 0 || c->post_sweeps < 0) fail(TMG_ERR_CONFIG, "smoothing sweep counts must be non-negative");
+    if (c->pre_sweeps != c->post_sweeps)
+      fail(TMG_ERR_CONFIG, "pcgmg needs pre_sweeps == post_sweeps for a symmetric preconditioner");
+    for (int i = 0; i < np; ++i)
+      if (!(c->phase_moduli[i] > 0.0))
+        fail(TMG_ERR_CONFIG, "phase modulus " + std::to_string(i + 1) +
+                                 " must be positive (void is a small positive number)");
+    if (!(c->penalty >= 1.0)) fail(TMG_ERR_CONFIG, "penalty exponent must be >= 1, got " + std::to_string(c->penalty));
+
+    Rank& R = *h->ranks[0];
+    const Grid& g = R.fine().g;
+    const long ne = static_cast<long>(g.nx) * g.ny, nv = ne * np;
+    const int blocks = oc_blocks();
+    // device state: density, the density before the OC sweep (and before each
+    // inner sweep), last deltas, move limits, energies + raw and filtered
+    // sensitivities, phase moduli and fractions, then the OC scratch
+    double* scratch = oc_scratch(R, ne, 0, blocks);
+    const long sz = 5 * nv + 2 * ne + nv + 2L * np + 2;
+    double* base = grow(R.dense, R.dense_cap, sz);
+    double* dens = base;
+    double* before = dens + nv;
+    double* pre = before + nv;
+    double* last = pre + nv;
+    double* filt = last + nv;
+    double* move = filt + nv;
+    double* en = move + ne;
+    double* raw = en + ne;
+    double* pm = raw + nv;
+    double* fr = pm + np;
+    auto* maxbits = reinterpret_cast<unsigned long long*>(fr + np);
+    CK(cudaMemcpyAsync(pm, c->phase_moduli, sizeof(double) * np, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(fr, c->volume_fractions, sizeof(double) * np, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemsetAsync(last, 0, sizeof(double) * nv, h->stream));
+    k_fill_uniform<<<1184, 256, 0, h->stream>>>(ne, np, fr, dens);
+    CKL();
+    std::vector<double> mv_host(static_cast<size_t>(ne), c->move_limit);
+    CK(cudaMemcpyAsync(move, mv_host.data(), sizeof(double) * ne, cudaMemcpyHostToDevice, h->stream));
+    for (Rank* Rk : h->ranks) upload_nodes(h->stream, Rk->b, rhs, Rk->fine().g);
+    h->count();
+    auto max_change = [&](const double* a, const double* b) {
+      CK(cudaMemsetAsync(maxbits, 0, sizeof(unsigned long long), h->stream));
+      k_max_abs_diff<<<1184, 256, 0, h->stream>>>(nv, a, b, maxbits);
+      CKL();
+      h->count();
+      unsigned long long bits = 0;
+      CK(cudaMemcpyAsync(R.scal_host, maxbits, sizeof(bits), cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      std::memcpy(&bits, R.scal_host, sizeof(bits));
+      double v;
+      std::memcpy(&v, &bits, sizeof(v));
+      return v;
+    };
+    auto chk = [&](int st) {
+      if (st != TMG_OK) fail(st, h->err, h->err_row);
+    };
+    *outer_iterations = 0;
+    *total_solver_iterations = 0;
+    *converged = 0;
+    bool have_u = false;
+    const int reach = static_cast<int>(std::ceil(c->filter_radius)) - 1;
+    for (int outer = 1; outer <= c->max_outer; ++outer) {
+      const auto t_iter = clk::now();
+      // assemble_elasticity + build_multigrid_operators (mto.cpp:267-281)
+      k_simp<<<dim3((g.ny + 127) / 128, g.nx), 128, 0, h->stream>>>(g, np, dens, pm, c->penalty, R.E);
+      CKL();
+      h->count();
+      h->have_moduli = true;
+      h->have_setup = false;
+      setup(h, c->omega);
+      // pcgmg_solve, warm-started from the previous u (mto.cpp:268-283)
+      const bool warm = c->warm_start && have_u;
+      if (warm)
+        CK(cudaMemcpyAsync(R.x0, R.x, sizeof(double2) * g.size, cudaMemcpyDeviceToDevice, h->stream));
+      SolveOut o;
+      solve_resident(h, warm, c->solver_tol, c->solver_max_iter, c->gamma, c->pre_sweeps, c->post_sweeps, o);
+      have_u = true;
+      double comp = 0.0;
+      chk(tmg_gpu_compliance(h, nullptr, &comp));
+      compliance_hist[outer - 1] = comp;
+      iters_hist[outer - 1] = o.iterations;
+      *total_solver_iterations += o.iterations;
+      // sensitivities and filtered sensitivities (mto.cpp:61-117, 300-310)
+      k_element_energy<<<dim3((g.ny + 127) / 128, g.nx), 128, 0, h->stream>>>(g, R.x, en);
+      CKL();
+      k_sensitivity<<<1184, 256, 0, h->stream>>>(ne, np, dens, en, pm, c->penalty, raw);
+      CKL();
+      h->count(2);
+      for (int i = 0; i < np; ++i) {
+        if (c->filter_radius <= 1.0) {
+          CK(cudaMemcpyAsync(filt + i * ne, raw + i * ne, sizeof(double) * ne, cudaMemcpyDeviceToDevice, h->stream));
+        } else {
+          k_filter<<<dim3((g.ny + 127) / 128, g.nx), 128, 0, h->stream>>>(g.nx, g.ny, np, i, c->filter_radius, reach,
+                                                                           dens, raw + i * ne, filt + i * ne);
+          CKL();
+          h->count();
+        }
+      }
+      // OC pair sweeps (mto.cpp:312-323)
+      CK(cudaMemcpyAsync(before, dens, sizeof(double) * nv, cudaMemcpyDeviceToDevice, h->stream));
+      for (int a = 0; a < np - 1; ++a)
+        for (int b = a + 1; b < np; ++b)
+          for (int sweep = 0; sweep < c->inner_sweeps; ++sweep) {
+            if (c->inner_sweeps > 1)
+              CK(cudaMemcpyAsync(pre, dens, sizeof(double) * nv, cudaMemcpyDeviceToDevice, h->stream));
+            oc_pair_device(h, R, scratch, dens, ne, np, c->density_floor, a, b, filt + a * ne, filt + b * ne,
+                           c->volume_fractions[a], move, c->oc_damping);
+            // with one sweep the reference's stop test cannot change anything
+            if (c->inner_sweeps == 1 || max_change(dens, pre) <= c->filter_tol) break;
+          }
+      // move limits and the convergence test (mto.cpp:325-350)
+      k_move_adapt<<<1184, 256, 0, h->stream>>>(ne, np, dens, before, last, move, c->move_limit);
+      CKL();
+      h->count();
+      const double change = max_change(dens, before);
+      change_hist[outer - 1] = change;
+      seconds_hist[outer - 1] = std::chrono::duration<double>(clk::now() - t_iter).count();
+      *outer_iterations = outer;
+      if (change <= c->tol) {
+        *converged = 1;
+        break;
+      }
+    }
+    CK(cudaMemcpyAsync(density_out, dens, sizeof(double) * nv, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    *seconds = std::chrono::duration<double>(clk::now() - t_start).count();
   });
 }
 

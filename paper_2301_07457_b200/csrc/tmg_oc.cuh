@@ -208,3 +208,50 @@ __global__ void __launch_bounds__(kOcThreads) k_oc_bisect(OcArgs a, int prep_blo
 }
 
 }  // namespace tmg
+
+namespace tmg {
+
+// ------------------------------------------ optimizer loop (mto.cpp:229-354)
+
+// DensityField::uniform (density.cpp:33-42)
+__global__ void k_fill_uniform(long ne, int np, const double* __restrict__ fractions, double* __restrict__ alpha) {
+  for (long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; k < ne * np;
+       k += static_cast<long>(gridDim.x) * blockDim.x)
+    alpha[k] = fractions[k % np];
+}
+
+// DensityField::max_change (density.cpp:60-66) into *out as the bits of a
+// non-negative double (uint64 order = double order: the max is exact and
+// independent of the order of the atomics)
+__global__ void k_max_abs_diff(long n, const double* __restrict__ a, const double* __restrict__ b,
+                               unsigned long long* out) {
+  double m = 0.0;
+  for (long k = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<long>(gridDim.x) * blockDim.x)
+    m = s_max(m, fabs(a[k] - b[k]));
+  for (int o = 16; o > 0; o >>= 1) m = s_max(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
+// per-element move limits: halved when a phase's change reverses, regrown by
+// 5 % on a consistent move (mto.cpp:325-343)
+__global__ void k_move_adapt(long ne, int np, const double* __restrict__ after, const double* __restrict__ before,
+                             double* __restrict__ last, double* __restrict__ move, double move_limit) {
+  for (long e = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; e < ne;
+       e += static_cast<long>(gridDim.x) * blockDim.x) {
+    bool flipped = false, moved = false;
+    for (int i = 0; i < np; ++i) {
+      const double delta = after[e * np + i] - before[e * np + i];
+      const double l = last[e * np + i];
+      if (fabs(delta) > 1e-12) moved = true;
+      if (delta * l < -1e-12) flipped = true;
+      last[e * np + i] = delta;
+    }
+    double mv = move[e];
+    if (flipped) mv = s_max(1e-4, 0.5 * mv);
+    else if (moved) mv = s_min(move_limit, 1.05 * mv);
+    move[e] = mv;
+  }
+}
+
+}  // namespace tmg

@@ -490,4 +490,66 @@ def oc_timings(ops: MultigridOperators):
     return ms.value, steps.value
 
 
+@dataclass
+class OptimConfig:
+    """OptimConfig (mto.hpp:12-27); the solver method is pcgmg."""
+    volume_fractions: list = field(default_factory=lambda: [0.15, 0.15, 0.15, 0.55])
+    filter_radius: float = 8.0
+    filter_tol: float = 0.05
+    tol: float = 1e-3
+    inner_sweeps: int = 1
+    move_limit: float = 0.2
+    oc_damping: float = 0.5
+    warm_start: bool = False
+    max_outer: int = 2000
+    density_floor: float = 1e-3
+    solver: SolverConfig = field(default_factory=SolverConfig)
+
+
+@dataclass
+class OptimReport:
+    """OptimReport (mto.hpp:29-39); density is element-major [ne, nphases]."""
+    density: np.ndarray
+    compliance_history: list
+    change_history: list
+    solver_iteration_history: list
+    seconds_history: list
+    outer_iterations: int
+    total_solver_iterations: int
+    seconds: float
+    converged: bool
+
+
+def optimize(ops: MultigridOperators, material: MaterialModel, cfg: OptimConfig,
+             rhs: np.ndarray | None = None) -> OptimReport:
+    """optimize() with Method::pcgmg (mto.cpp:229-354), every per-iteration
+    step on the device. ops carries the grid, the supports and Poisson's
+    ratio; rhs defaults to the wall problem's uniform top load."""
+    if rhs is None:
+        rhs = assemble_rhs(ops.grid, wall_boundary_conditions(ops.grid, "uniform"))
+    b = np.ascontiguousarray(rhs, dtype=np.float64)
+    if b.size != ops.grid.dof_count():
+        raise DimensionError("optimize: rhs length does not match the grid")
+    pm = np.ascontiguousarray(material.phase_moduli, dtype=np.float64)
+    fr = np.ascontiguousarray(cfg.volume_fractions, dtype=np.float64)
+    if fr.size != pm.size:
+        raise ConfigError(f"volume fraction count {fr.size} does not match phase count {pm.size}")
+    from ._lib import OptimConfigC
+    s = cfg.solver
+    c = OptimConfigC(pm.size, dptr(pm), material.penalty, dptr(fr), cfg.filter_radius, cfg.filter_tol, cfg.tol,
+                     cfg.inner_sweeps, cfg.move_limit, cfg.oc_damping, int(cfg.warm_start), cfg.max_outer,
+                     cfg.density_floor, s.tol, s.max_iter, s.gamma, s.pre_sweeps, s.post_sweeps, s.omega)
+    ne, m = ops.grid.element_count(), max(cfg.max_outer, 1)
+    dens = np.empty((ne, pm.size))
+    ch, dh, sh = np.zeros(m), np.zeros(m), np.zeros(m)
+    ih = np.zeros(m, dtype=np.int32)
+    oi, cv = C.c_int(), C.c_int()
+    ti, sec = C.c_long(), C.c_double()
+    ops._check(ops.lib.tmg_gpu_optimize(ops.h, C.byref(c), dptr(b), dptr(dens), dptr(ch), dptr(dh), iptr(ih),
+                                        dptr(sh), C.byref(oi), C.byref(ti), C.byref(cv), C.byref(sec)))
+    k = oi.value
+    return OptimReport(dens, list(ch[:k]), list(dh[:k]), [int(v) for v in ih[:k]], list(sh[:k]), k, ti.value,
+                       sec.value, bool(cv.value))
+
+
 __all__ = [n for n in dir() if not n.startswith("_") and n not in ("C", "dataclasses", "np", "dataclass", "field")]

@@ -130,6 +130,23 @@ def main():
         print(name, "iterations", r["iterations"])
         oc_cases(name, floored, d["filter_r1.5"], seed, oc)
     np.savez_compressed(OUT / "oc_pair.npz", **oc)
+    optim_cases()
+
+
+def optim_cases():
+    """optimize() with Method::pcgmg (mto.cpp:229-354) on two c0-style wall
+    problems: BASELINE config-0 materials and fractions, uniform top load."""
+    out = {}
+    for tag, n, kw in (("n16", 16, dict(filter_radius=1.5, max_outer=8, num_coarsenings=1)),
+                       ("n24_warm", 24, dict(filter_radius=3.0, max_outer=6, num_coarsenings=1, warm_start=True,
+                                             inner_sweeps=2))):
+        fixed, loads = wall(n, n, "uniform")
+        r = po.optimize("ref", n, n, fixed, loads, PHASES, 3.0, 0.3, [0.15, 0.15, 0.15, 0.55], tol=1e-12, **kw)
+        for k, v in r.items():
+            out[f"{tag}_{k}"] = np.asarray(v)
+        out[f"{tag}_args"] = np.array([n, kw["filter_radius"], kw["max_outer"], kw["num_coarsenings"],
+                                       int(kw.get("warm_start", False)), kw.get("inner_sweeps", 1)])
+    np.savez_compressed(OUT / "optimize.npz", **out)
 
 
 def oc_cases(name, alpha, filt, seed, out):

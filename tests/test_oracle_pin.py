@@ -183,3 +183,38 @@ def test_oc_update_pair_matches_live_reference():
         r1, s1 = po.oc_update_pair("ref", a, 0, nph - 1, sa, sb, target, move, 0.3 + 0.1 * trial)
         r2, s2 = po.oc_update_pair("orc", a, 0, nph - 1, sa, sb, target, move, 0.3 + 0.1 * trial)
         assert s1 == s2 and np.array_equal(r1, r2)
+
+
+def _wall(n):
+    fixed, loads = [], []
+    for x in range(n + 1):
+        node = x * (n + 1)
+        fixed += [2 * node, 2 * node + 1]
+        loads.append((2 * (x * (n + 1) + n) + 1, -1.0 / (n + 1)))
+    return fixed, loads
+
+
+def test_optimize_golden_bit_exact():
+    """The whole optimizer loop (mto.cpp:229-354) against the reference's own
+    OptimReport: density and every history bit for bit."""
+    d = np.load(GOLDEN / "optimize.npz")
+    for tag in ("n16", "n24_warm"):
+        n, radius, max_outer, nc, warm, sweeps = d[tag + "_args"]
+        fixed, loads = _wall(int(n))
+        r = po.optimize("orc", int(n), int(n), fixed, loads, PHASES, 3.0, 0.3, [0.15, 0.15, 0.15, 0.55],
+                        filter_radius=float(radius), tol=1e-12, max_outer=int(max_outer), num_coarsenings=int(nc),
+                        warm_start=bool(warm), inner_sweeps=int(sweeps))
+        for k in ("density", "compliance_history", "change_history", "solver_iteration_history",
+                  "outer_iterations", "total_solver_iterations", "converged"):
+            assert np.array_equal(np.asarray(r[k]), d[f"{tag}_{k}"]), (tag, k)
+
+
+def test_optimize_matches_live_reference():
+    if not po.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    fixed, loads = _wall(20)
+    kw = dict(filter_radius=2.0, tol=1e-3, max_outer=5, num_coarsenings=1, move_limit=0.1, oc_damping=0.7)
+    a = po.optimize("ref", 20, 20, fixed, loads, PHASES, 3.0, 0.3, [0.2, 0.1, 0.1, 0.6], **kw)
+    b = po.optimize("orc", 20, 20, fixed, loads, PHASES, 3.0, 0.3, [0.2, 0.1, 0.1, 0.6], **kw)
+    for k in a:
+        assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
