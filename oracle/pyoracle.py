@@ -267,3 +267,29 @@ def optimize(kind, nx, ny, fixed, loads, phase_moduli, penalty, nu, fractions, f
     return dict(density=dens.reshape(nx * ny, np_), compliance_history=ch[:k], change_history=dh[:k],
                 solver_iteration_history=ih[:k], outer_iterations=k, total_solver_iterations=ti.value,
                 converged=bool(cv.value))
+
+
+def ref_write_history_csv(report, path):
+    """The reference's write_history_csv (report.cpp:34-43) on an OptimReport-like object."""
+    n = len(report.compliance_history)
+    c = np.ascontiguousarray(report.compliance_history, dtype=np.float64)
+    d = np.ascontiguousarray(report.change_history, dtype=np.float64)
+    it = np.ascontiguousarray(report.solver_iteration_history, dtype=np.int32)
+    s = np.ascontiguousarray(report.seconds_history, dtype=np.float64)
+    st = lib("ref").ref_write_history_csv(n, _d(c), _d(d), it.ctypes.data_as(_I), _d(s), str(path).encode())
+    if st:
+        raise OracleError(st, "write_history_csv")
+
+
+def ref_write_residual_csv(hist, path):
+    h = np.ascontiguousarray(hist, dtype=np.float64)
+    st = lib("ref").ref_write_residual_csv(len(h), _d(h), str(path).encode())
+    if st:
+        raise OracleError(st, "write_residual_csv")
+
+
+def ref_write_density_images(nx, ny, alpha, directory):
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    st = lib("ref").ref_write_density_images(nx, ny, a.shape[1], _d(a), str(directory).encode())
+    if st:
+        raise OracleError(st, "write images")

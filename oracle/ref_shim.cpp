@@ -25,6 +25,7 @@
 #include "topmg/fem.hpp"
 #include "topmg/grid.hpp"
 #include "topmg/mto.hpp"
+#include "topmg/report.hpp"
 #include "topmg/solvers.hpp"
 #include "topmg/sparse.hpp"
 
@@ -376,6 +377,46 @@ int ref_optimize(int nx, int ny, int np, const double* pm, double penalty, doubl
     return 0;
   } catch (...) {
     return map_exception(err, errlen, nullptr);
+  }
+}
+
+// report.cpp:34-97: the reference's own output writers, for byte-compatibility
+// tests of the Python mirror's writers
+int ref_write_history_csv(int n, const double* compliance, const double* change, const int* iters,
+                          const double* seconds, const char* path) {
+  try {
+    topmg::OptimReport r;
+    r.compliance_history.assign(compliance, compliance + n);
+    r.change_history.assign(change, change + n);
+    r.solver_iteration_history.assign(iters, iters + n);
+    r.seconds_history.assign(seconds, seconds + n);
+    topmg::write_history_csv(r, path);
+    return 0;
+  } catch (...) {
+    return map_exception(nullptr, 0, nullptr);
+  }
+}
+
+int ref_write_residual_csv(int n, const double* hist, const char* path) {
+  try {
+    topmg::SolveReport r;
+    r.residual_history.assign(hist, hist + n);
+    topmg::write_residual_csv(r, path);
+    return 0;
+  } catch (...) {
+    return map_exception(nullptr, 0, nullptr);
+  }
+}
+
+int ref_write_density_images(int nx, int ny, int nphases, const double* alpha, const char* dir) {
+  try {
+    topmg::DensityField d = make_density(nx, ny, nphases, alpha);
+    for (int i = 0; i < nphases; ++i)
+      topmg::write_phase_pgm(d, i, std::string(dir) + "/phase_" + std::to_string(i + 1) + ".pgm");
+    topmg::write_composite_ppm(d, std::string(dir) + "/composite.ppm");
+    return 0;
+  } catch (...) {
+    return map_exception(nullptr, 0, nullptr);
   }
 }
 

@@ -27,6 +27,7 @@ from .topmg import (  # noqa: F401
     density_checker,
     density_iid,
     effective_moduli,
+    emit_outputs,
     element_energies,
     element_stiffness,
     filter_sensitivities,
@@ -41,4 +42,8 @@ from .topmg import (  # noqa: F401
     sensitivities,
     slab_partition,
     wall_boundary_conditions,
+    write_composite_ppm,
+    write_history_csv,
+    write_phase_pgm,
+    write_residual_csv,
 )

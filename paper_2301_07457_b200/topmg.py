@@ -552,4 +552,75 @@ def optimize(ops: MultigridOperators, material: MaterialModel, cfg: OptimConfig,
                        sec.value, bool(cv.value))
 
 
+# ------------------------------------------------------------- outputs --
+# Byte-compatible with the reference writers (report.cpp:34-97, 153-168);
+# host-side, like the reference's.
+
+def _fmt(v: float) -> str:
+    return "%.17g" % v  # report.cpp:17-19
+
+
+def _to_byte(a: np.ndarray) -> np.ndarray:
+    """report.cpp:28-31: clamp(lround(255 a), 0, 255), lround = half away from zero."""
+    x = 255.0 * np.asarray(a, dtype=np.float64)
+    fl = np.floor(x)
+    r = np.where(x - fl >= 0.5, fl + 1.0, fl)  # x >= 0 here; negatives clamp to 0 anyway
+    return np.clip(r, 0, 255).astype(np.uint8)
+
+
+def write_history_csv(report: OptimReport, path) -> None:
+    with open(path, "w", newline="") as out:
+        out.write("iteration,compliance,max_change,solver_iterations,seconds\n")
+        for i in range(len(report.compliance_history)):
+            out.write(f"{i + 1},{_fmt(report.compliance_history[i])},{_fmt(report.change_history[i])},"
+                      f"{int(report.solver_iteration_history[i])},{_fmt(report.seconds_history[i])}\n")
+
+
+def write_residual_csv(report: SolveReport, path) -> None:
+    with open(path, "w", newline="") as out:
+        out.write("iteration,relative_residual\n")
+        for i, v in enumerate(report.residual_history):
+            out.write(f"{i},{_fmt(v)}\n")
+
+
+def _image_rows(alpha: np.ndarray, nx: int, ny: int) -> np.ndarray:
+    """[ny, nx, nphases], top row first (report.cpp:55-57: ey = ny-1 .. 0)."""
+    return np.asarray(alpha, dtype=np.float64).reshape(nx, ny, -1).transpose(1, 0, 2)[::-1]
+
+
+def write_phase_pgm(alpha: np.ndarray, nx: int, ny: int, phase: int, path) -> None:
+    img = _to_byte(_image_rows(alpha, nx, ny)[:, :, phase])
+    with open(path, "wb") as out:
+        out.write(f"P5\n{nx} {ny}\n255\n".encode())
+        out.write(img.tobytes())
+
+
+def write_composite_ppm(alpha: np.ndarray, nx: int, ny: int, path) -> None:
+    a = _image_rows(alpha, nx, ny)
+    nph = a.shape[2]
+    rgb = np.zeros(a.shape[:2] + (3,))
+    for i in range(nph):  # void (last) and phases beyond the third render gray
+        if i < 3 and i != nph - 1:
+            rgb[:, :, i] += a[:, :, i]
+        else:
+            rgb += a[:, :, i:i + 1]
+    img = _to_byte(np.minimum(1.0, rgb))
+    with open(path, "wb") as out:
+        out.write(f"P6\n{nx} {ny}\n255\n".encode())
+        out.write(img.tobytes())
+
+
+def emit_outputs(report: OptimReport, grid: GridLevel, out_dir, images: bool = True, csv: bool = True) -> None:
+    """emit_outputs (report.cpp:153-168): history.csv, phase_<i>.pgm, composite.ppm."""
+    import os
+
+    os.makedirs(out_dir, exist_ok=True)
+    if csv:
+        write_history_csv(report, os.path.join(out_dir, "history.csv"))
+    if images:
+        for i in range(report.density.shape[1]):
+            write_phase_pgm(report.density, grid.nx, grid.ny, i, os.path.join(out_dir, f"phase_{i + 1}.pgm"))
+        write_composite_ppm(report.density, grid.nx, grid.ny, os.path.join(out_dir, "composite.ppm"))
+
+
 __all__ = [n for n in dir() if not n.startswith("_") and n not in ("C", "dataclasses", "np", "dataclass", "field")]
