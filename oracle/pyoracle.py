@@ -181,6 +181,25 @@ class System:
             pass
 
 
+def poisson_system(kind, nx, ny, source):
+    """assemble_poisson (fem.cpp:232-276) as a System (1 dof per node); source is
+    a per-node array or a constant."""
+    src = np.ascontiguousarray(np.broadcast_to(np.asarray(source, dtype=np.float64), ((nx + 1) * (ny + 1),)))
+    s = System.__new__(System)
+    s.kind, s.p, s.nx, s.ny = kind, kind + "_", nx, ny
+    s.L = lib(kind)
+    s.n = (nx + 1) * (ny + 1)
+    s.levels = 1
+    err = C.create_string_buffer(256)
+    st = C.c_int()
+    f = getattr(s.L, kind + "_poisson_create")
+    f.restype = C.c_void_p
+    s.h = f(nx, ny, _d(src), err, 256, C.byref(st))
+    if st.value:
+        raise OracleError(st.value, err.value.decode())
+    return s
+
+
 def element_stiffness(kind, modulus, nu):
     k = np.empty(64)
     getattr(lib(kind), kind + "_element_stiffness")(modulus, nu, _d(k))

@@ -116,11 +116,28 @@ void* ref_system_create(int nx, int ny, const double* moduli, double nu,
   }
 }
 
+// assemble_poisson (fem.cpp:232-276): the Poisson system on a 1-dof grid
+void* ref_poisson_create(int nx, int ny, const double* source, char* err, int errlen, int* status) {
+  try {
+    auto s = std::make_unique<RefSystem>();
+    s->grid = topmg::GridLevel{nx, ny, 1, 0};
+    std::vector<double> f(source, source + static_cast<std::size_t>(nx + 1) * (ny + 1));
+    const auto t0 = Clock::now();
+    s->sys = topmg::assemble_poisson(s->grid, f);
+    s->t_assemble = std::chrono::duration<double>(Clock::now() - t0).count();
+    *status = 0;
+    return s.release();
+  } catch (...) {
+    *status = map_exception(err, errlen, nullptr);
+    return nullptr;
+  }
+}
+
 int ref_system_build_mg(void* h, int num_coarsenings, double omega, char* err,
                         int errlen, int* row) {
   auto* s = static_cast<RefSystem*>(h);
   try {
-    s->hier = topmg::build_hierarchy(s->grid.nx, s->grid.ny, num_coarsenings, 2);
+    s->hier = topmg::build_hierarchy(s->grid.nx, s->grid.ny, num_coarsenings, s->grid.dofs_per_node);
     const auto t0 = Clock::now();
     s->ops = std::make_unique<topmg::MultigridOperators>(
         topmg::build_multigrid_operators(s->hier, s->sys.matrix, omega));

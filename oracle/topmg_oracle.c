@@ -127,10 +127,10 @@ typedef struct {
   double* w;
 } Prol;
 
-static void prol_build(Prol* p, Lvl coarse, Lvl fine) {
-  const int nf = 2 * lvl_nodes(fine);
+static void prol_build(Prol* p, Lvl coarse, Lvl fine, int dpn) {
+  const int nf = dpn * lvl_nodes(fine);
   p->nf = nf;
-  p->nc = 2 * lvl_nodes(coarse);
+  p->nc = dpn * lvl_nodes(coarse);
   p->off = malloc(sizeof(int) * (size_t)(nf + 1));
   p->par = malloc(sizeof(int) * (size_t)nf * 4);
   p->w = malloc(sizeof(double) * (size_t)nf * 4);
@@ -144,10 +144,10 @@ static void prol_build(Prol* p, Lvl coarse, Lvl fine) {
       py[0] = fy / 2; py[1] = fy / 2 + 1;
       if (fx % 2) { mx = 2; wx[0] = wx[1] = 0.5; } else { mx = 1; wx[0] = 1.0; }
       if (fy % 2) { my = 2; wy[0] = wy[1] = 0.5; } else { my = 1; wy[0] = 1.0; }
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < dpn; ++c) {
         for (int a = 0; a < mx; ++a)
           for (int b = 0; b < my; ++b) {
-            p->par[k] = (px[a] * (coarse.ny + 1) + py[b]) * 2 + c;
+            p->par[k] = (px[a] * (coarse.ny + 1) + py[b]) * dpn + c;
             p->w[k] = wx[a] * wy[b];
             ++k;
           }
@@ -245,7 +245,7 @@ static int assemble(int nx, int ny, const double* E, const double* ke,
 
 /* Galerkin (1/4) P^T A P on the nine-point coarse pattern, accumulated in
  * the reference's loop order: solvers.cpp:397-458 */
-static void galerkin(const Csr* a, const Prol* p, Lvl cl, Csr* out) {
+static void galerkin(const Csr* a, const Prol* p, Lvl cl, Csr* out, int dpn) {
   const int nc = p->nc;
   out->n = nc;
   out->off = malloc(sizeof(int) * (size_t)(nc + 1));
@@ -254,16 +254,16 @@ static void galerkin(const Csr* a, const Prol* p, Lvl cl, Csr* out) {
   out->off[0] = 0;
   for (int x = 0; x <= cl.nx; ++x)
     for (int y = 0; y <= cl.ny; ++y)
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < dpn; ++c) {
         /* neighbor dofs ascending: node index grows with x then y */
         for (int x2 = x - 1; x2 <= x + 1; ++x2) {
           if (x2 < 0 || x2 > cl.nx) continue;
           for (int y2 = y - 1; y2 <= y + 1; ++y2) {
             if (y2 < 0 || y2 > cl.ny) continue;
-            for (int d = 0; d < 2; ++d) out->col[k++] = 2 * (x2 * (cl.ny + 1) + y2) + d;
+            for (int d = 0; d < dpn; ++d) out->col[k++] = dpn * (x2 * (cl.ny + 1) + y2) + d;
           }
         }
-        out->off[2 * (x * (cl.ny + 1) + y) + c + 1] = k;
+        out->off[dpn * (x * (cl.ny + 1) + y) + c + 1] = k;
       }
   out->val = calloc((size_t)k, sizeof(double));
   for (int i = 0; i < p->nf; ++i) {
@@ -364,6 +364,7 @@ static void chol_free(Chol* f) {
 
 typedef struct {
   int nx, ny, n;
+  int dpn; /* dofs per node: 2 elasticity, 1 Poisson */
   double nu, omega;
   Csr fine;
   double* rhs;
@@ -409,6 +410,7 @@ void* orc_system_create(int nx, int ny, const double* moduli, double nu,
   s->nx = nx;
   s->ny = ny;
   s->n = n;
+  s->dpn = 2;
   s->nu = nu;
   double ke[64];
   orc_element_stiffness(1.0, nu, ke);
@@ -462,9 +464,9 @@ int orc_system_build_mg(void* h, int nc, double omega, char* err, int errlen, in
     s->lv[l].nx = s->nx >> (nc - l);
     s->lv[l].ny = s->ny >> (nc - l);
   }
-  for (int l = 1; l <= nc; ++l) prol_build(&s->pr[l - 1], s->lv[l - 1], s->lv[l]);
+  for (int l = 1; l <= nc; ++l) prol_build(&s->pr[l - 1], s->lv[l - 1], s->lv[l], s->dpn);
   s->mat[nc] = s->fine;
-  for (int l = nc; l >= 1; --l) galerkin(&s->mat[l], &s->pr[l - 1], s->lv[l - 1], &s->mat[l - 1]);
+  for (int l = nc; l >= 1; --l) galerkin(&s->mat[l], &s->pr[l - 1], s->lv[l - 1], &s->mat[l - 1], s->dpn);
   int bad = -1;
   double piv = 0.0;
   const int st = chol_factor(&s->mat[0], &s->coarse, &bad, &piv);
@@ -980,4 +982,108 @@ int orc_optimize(int nx, int ny, int np, const double* pm, double penalty, doubl
   free(raw);
   free(filt);
   return st;
+}
+
+/* ------------------------------------------------------------- poisson -- */
+
+/* poisson_element_matrix / poisson_mass_matrix: 2x2 Gauss on the unit
+ * square, upper triangle accumulated then mirrored (fem.cpp:37-81) */
+void orc_poisson_matrices(double* k, double* m) {
+  const double g = 0.57735026918962576451;
+  const double pts[2] = {-g, g};
+  memset(k, 0, 16 * sizeof(double));
+  memset(m, 0, 16 * sizeof(double));
+  for (int qa = 0; qa < 2; ++qa)
+    for (int qb = 0; qb < 2; ++qb) {
+      const double xi = pts[qa], eta = pts[qb];
+      const double dx[4] = {2.0 * (-(1.0 - eta) / 4.0), 2.0 * ((1.0 - eta) / 4.0), 2.0 * ((1.0 + eta) / 4.0),
+                            2.0 * (-(1.0 + eta) / 4.0)};
+      const double dy[4] = {2.0 * (-(1.0 - xi) / 4.0), 2.0 * (-(1.0 + xi) / 4.0), 2.0 * ((1.0 + xi) / 4.0),
+                            2.0 * ((1.0 - xi) / 4.0)};
+      const double nv[4] = {(1.0 - xi) * (1.0 - eta) / 4.0, (1.0 + xi) * (1.0 - eta) / 4.0,
+                            (1.0 + xi) * (1.0 + eta) / 4.0, (1.0 - xi) * (1.0 + eta) / 4.0};
+      for (int i = 0; i < 4; ++i)
+        for (int j = i; j < 4; ++j) {
+          k[i * 4 + j] += 0.25 * (dx[i] * dx[j] + dy[i] * dy[j]);
+          m[i * 4 + j] += 0.25 * nv[i] * nv[j];
+        }
+    }
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < i; ++j) {
+      k[i * 4 + j] = k[j * 4 + i];
+      m[i * 4 + j] = m[j * 4 + i];
+    }
+}
+
+/* assemble_poisson (fem.cpp:232-276): the Q4 Laplacian with the consistent
+ * load -M f, every boundary node fixed (identity row, rhs 0) */
+void* orc_poisson_create(int nx, int ny, const double* source, char* err, int errlen, int* status) {
+  (void)err;
+  (void)errlen;
+  const double t0 = now_s();
+  const int n = (nx + 1) * (ny + 1);
+  double k[16], m[16];
+  orc_poisson_matrices(k, m);
+  int* fc = calloc((size_t)n, sizeof(int));
+  for (int x = 0; x <= nx; ++x)
+    for (int y = 0; y <= ny; ++y)
+      if (x == 0 || y == 0 || x == nx || y == ny) fc[x * (ny + 1) + y] = 1;
+  Sys* s = calloc(1, sizeof(Sys));
+  s->nx = nx;
+  s->ny = ny;
+  s->n = n;
+  s->dpn = 1;
+  Csr* out = &s->fine;
+  out->n = n;
+  out->off = malloc(sizeof(int) * (size_t)(n + 1));
+  out->col = malloc(sizeof(int) * (size_t)n * 9);
+  out->val = malloc(sizeof(double) * (size_t)n * 9);
+  int q = 0;
+  out->off[0] = 0;
+  for (int x = 0; x <= nx; ++x)
+    for (int y = 0; y <= ny; ++y) {
+      const int row = x * (ny + 1) + y;
+      if (fc[row]) {
+        out->col[q] = row;
+        out->val[q++] = 1.0;
+        out->off[row + 1] = q;
+        continue;
+      }
+      for (int x2 = x - 1; x2 <= x + 1; ++x2) {
+        if (x2 < 0 || x2 > nx) continue;
+        for (int y2 = y - 1; y2 <= y + 1; ++y2) {
+          if (y2 < 0 || y2 > ny) continue;
+          const int colid = x2 * (ny + 1) + y2;
+          if (fc[colid]) continue;
+          double v = 0.0;
+          for (int ex = x - 1; ex <= x; ++ex) {
+            if (ex < 0 || ex >= nx || x2 - ex < 0 || x2 - ex > 1) continue;
+            for (int ey = y - 1; ey <= y; ++ey) {
+              if (ey < 0 || ey >= ny || y2 - ey < 0 || y2 - ey > 1) continue;
+              v += k[corner(x - ex, y - ey) * 4 + corner(x2 - ex, y2 - ey)];
+            }
+          }
+          out->col[q] = colid;
+          out->val[q++] = v;
+        }
+      }
+      out->off[row + 1] = q;
+    }
+  s->rhs = calloc((size_t)n, sizeof(double));
+  for (int ex = 0; ex < nx; ++ex)
+    for (int ey = 0; ey < ny; ++ey) {
+      const int nd[4] = {ex * (ny + 1) + ey, (ex + 1) * (ny + 1) + ey, (ex + 1) * (ny + 1) + ey + 1,
+                         ex * (ny + 1) + ey + 1};
+      for (int a = 0; a < 4; ++a) {
+        double load = 0.0;
+        for (int b = 0; b < 4; ++b) load += m[a * 4 + b] * source[nd[b]];
+        s->rhs[nd[a]] -= load;
+      }
+    }
+  for (int i = 0; i < n; ++i)
+    if (fc[i]) s->rhs[i] = 0.0;
+  free(fc);
+  s->t_asm = now_s() - t0;
+  *status = ST_OK;
+  return s;
 }

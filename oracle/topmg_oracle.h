@@ -73,6 +73,12 @@ int orc_filter(int nx, int ny, int nphases, const double* alpha, int phase,
 int orc_oc_update_pair(long ne, int nphases, double floor_eps, double* alpha, int phase_a,
                        int phase_b, const double* sens_a, const double* sens_b, double target,
                        const double* move, double damping);
+/* fem.cpp:37-81: the Q4 Laplacian and mass element matrices (4x4 each) */
+void orc_poisson_matrices(double* k16, double* m16);
+/* assemble_poisson (fem.cpp:232-276), 1 dof per node, every boundary node
+ * fixed; the returned system works with every orc_system_* call */
+void* orc_poisson_create(int nx, int ny, const double* node_source, char* err, int errlen,
+                         int* status);
 /* optimize() with Method::pcgmg (mto.cpp:229-354); density [ne * np] out,
  * histories of up to max_outer entries */
 int orc_optimize(int nx, int ny, int np, const double* phase_moduli, double penalty, double nu,

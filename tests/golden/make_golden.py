@@ -131,6 +131,38 @@ def main():
         oc_cases(name, floored, d["filter_r1.5"], seed, oc)
     np.savez_compressed(OUT / "oc_pair.npz", **oc)
     optim_cases()
+    poisson_cases()
+
+
+def full_depth(g):
+    d = 0
+    while g > 2:
+        g //= 2
+        d += 1
+    return d
+
+
+def poisson_cases():
+    """assemble_poisson + pcgmg (fem.cpp:232-276, bench.cpp:30-111): the
+    paper's Poisson bench setting (constant source 1, coarsest 2x2, omega 0.6,
+    2+2 sweeps, tol 1e-6) and a seeded random source."""
+    out = {}
+    for tag, g, src in (("g16", 16, 1.0), ("g64", 64, 1.0), ("g32_rand", 32, None)):
+        rng = np.random.default_rng(g)
+        source = rng.standard_normal((g + 1) ** 2) if src is None else np.full((g + 1) ** 2, src)
+        s = po.poisson_system("ref", g, g, source).build_mg(full_depth(g), 0.6)
+        b = s.rhs()
+        r = s.solve(b, tol=1e-6, max_iter=2000)
+        f = rng.standard_normal(s.n)
+        out[f"{tag}_source"], out[f"{tag}_b"] = source, b
+        out[f"{tag}_x"], out[f"{tag}_hist"] = r["solution"], r["residual_history"]
+        out[f"{tag}_iterations"] = np.array(r["iterations"])
+        out[f"{tag}_f"], out[f"{tag}_vcycle"] = f, s.vcycle(f, np.zeros(s.n), 1, 2, 2)
+        for lvl in range(full_depth(g) + 1):
+            off, col, val = s.csr(lvl)
+            out[f"{tag}_L{lvl}_off"], out[f"{tag}_L{lvl}_col"], out[f"{tag}_L{lvl}_val"] = off, col, val
+        s.close()
+    np.savez_compressed(OUT / "poisson.npz", **out)
 
 
 def optim_cases():

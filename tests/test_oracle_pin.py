@@ -218,3 +218,28 @@ def test_optimize_matches_live_reference():
     b = po.optimize("orc", 20, 20, fixed, loads, PHASES, 3.0, 0.3, [0.2, 0.1, 0.1, 0.6], **kw)
     for k in a:
         assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), k
+
+
+def _full_depth(g):
+    d = 0
+    while g > 2:
+        g //= 2
+        d += 1
+    return d
+
+
+@pytest.mark.parametrize("tag,g", [("g16", 16), ("g64", 64), ("g32_rand", 32)])
+def test_poisson_golden_bit_exact(tag, g):
+    """assemble_poisson + the Galerkin hierarchy + pcgmg on a 1-dof grid
+    (fem.cpp:232-276, bench.cpp:64-82) against the reference's own outputs."""
+    d = np.load(GOLDEN / "poisson.npz")
+    s = po.poisson_system("orc", g, g, d[tag + "_source"]).build_mg(_full_depth(g), 0.6)
+    assert np.array_equal(s.rhs(), d[tag + "_b"])
+    for lvl in range(_full_depth(g) + 1):
+        for got, key in zip(s.csr(lvl), ("off", "col", "val")):
+            assert np.array_equal(got, d[f"{tag}_L{lvl}_{key}"]), (lvl, key)
+    r = s.solve(d[tag + "_b"], tol=1e-6, max_iter=2000)
+    assert r["iterations"] == int(d[tag + "_iterations"])
+    assert np.array_equal(r["solution"], d[tag + "_x"])
+    assert np.array_equal(r["residual_history"], d[tag + "_hist"])
+    assert np.array_equal(s.vcycle(d[tag + "_f"], np.zeros(s.n), 1, 2, 2), d[tag + "_vcycle"])
