@@ -268,6 +268,37 @@ void tmg_inputs_wall_bc(int nx, int ny, int load_mode, int* fixed, int* n_fixed,
 void tmg_inputs_rhs(int nx, int ny, const int* fixed, int n_fixed,
                     const int* load_dofs, const double* load_vals, int n_loads,
                     double* b);
+/* poisson_element_matrix / poisson_mass_matrix (fem.cpp:37-81), row-major 4x4 */
+void tmg_poisson_element_matrices(double* k16, double* m16);
+/* the right-hand side of assemble_poisson (fem.cpp:243-276) for a per-node
+ * source: -M f assembled, boundary entries 0 */
+void tmg_inputs_poisson_rhs(int nx, int ny, const double* node_source, double* b);
+
+/* ---- Poisson pCGMG (tmg_poisson.cuh) -------------
+ * -lap(u) = -f on an nx x ny Q4 grid, 1 dof per node, every boundary node
+ * fixed (assemble_poisson, fem.cpp:232-276), solved by pcgmg_solve
+ * (solvers.cpp:516-530) with the Galerkin hierarchy of
+ * build_multigrid_operators (solvers.cpp:460-481) over
+ * build_hierarchy(nx, ny, num_coarsenings, 1). Single GPU. */
+typedef struct tmg_poisson_handle tmg_poisson_handle;
+int tmg_poisson_create(int nx, int ny, int num_coarsenings, int device,
+                       tmg_poisson_handle** out);
+void tmg_poisson_destroy(tmg_poisson_handle* h);
+int tmg_poisson_last_error(tmg_poisson_handle* h, char* buf, int len);
+/* assembles the fine operator on the device, the Galerkin levels and the
+ * coarsest inverse; omega is the Jacobi damping of the cycle */
+int tmg_poisson_setup(tmg_poisson_handle* h, double omega);
+/* level operator as 5 node-major planes (centre, N, SE, E, NE), each
+ * (nx_l+1)(ny_l+1) doubles in the reference node order */
+int tmg_poisson_level_values(tmg_poisson_handle* h, int level, double* planes);
+/* mg_cycle (solvers.cpp:483-514) at the finest level, u updated in place */
+int tmg_poisson_vcycle(tmg_poisson_handle* h, const double* f, double* u, int gamma,
+                       int pre_sweeps, int post_sweeps);
+/* pcgmg_solve with x0 (nullable); hist gets up to hist_cap entries */
+int tmg_poisson_solve(tmg_poisson_handle* h, const double* b, const double* x0, double tol,
+                      int max_iter, int gamma, int pre_sweeps, int post_sweeps, double* x,
+                      int* iterations, double* final_relres, int* converged, double* seconds,
+                      double* hist, int hist_cap, int* hist_len);
 
 #ifdef __cplusplus
 }

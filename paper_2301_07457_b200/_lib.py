@@ -60,6 +60,16 @@ SIGNATURES = [
     ("tmg_gpu_oc_update_pair", C.c_int,
      [_H, _D, C.c_int, C.c_double, C.c_int, C.c_int, _D, _D, C.c_double, _D, C.c_double]),
     ("tmg_gpu_oc_timings", C.c_int, [_H, _D, _I]),
+    ("tmg_poisson_create", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_H)]),
+    ("tmg_poisson_destroy", None, [_H]),
+    ("tmg_poisson_last_error", C.c_int, [_H, C.c_char_p, C.c_int]),
+    ("tmg_poisson_setup", C.c_int, [_H, C.c_double]),
+    ("tmg_poisson_level_values", C.c_int, [_H, C.c_int, _D]),
+    ("tmg_poisson_vcycle", C.c_int, [_H, _D, _D, C.c_int, C.c_int, C.c_int]),
+    ("tmg_poisson_solve", C.c_int, [_H, _D, _D, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, _D, _I, _D, _I,
+                                    _D, _D, C.c_int, _I]),
+    ("tmg_poisson_element_matrices", None, [_D, _D]),
+    ("tmg_inputs_poisson_rhs", None, [C.c_int, C.c_int, _D, _D]),
     ("tmg_gpu_optimize", C.c_int, [_H, C.POINTER(OptimConfigC), _D, _D, _D, _D, _I, _D, _I,
                                    C.POINTER(C.c_long), _I, _D]),
     ("tmg_gpu_apply", C.c_int, [_H, C.c_int, _D, _D]),

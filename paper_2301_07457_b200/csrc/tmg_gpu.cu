@@ -2175,3 +2175,5 @@ void tmg_host_free(void* p) {
 }
 
 }  // extern "C"
+
+#include "tmg_poisson.cuh"

@@ -157,4 +157,55 @@ void tmg_inputs_rhs(int nx, int ny, const int* fixed, int n_fixed, const int* lo
   for (int i = 0; i < n_fixed; ++i) b[fixed[i]] = 0.0;
 }
 
+// poisson_element_matrix / poisson_mass_matrix (fem.cpp:37-81): 2x2 Gauss
+// on the unit square, upper triangle accumulated then mirrored.
+void tmg_poisson_element_matrices(double* k16, double* m16) {
+  const double g = 0.57735026918962576451;
+  const double pts[2] = {-g, g};
+  std::memset(k16, 0, 16 * sizeof(double));
+  std::memset(m16, 0, 16 * sizeof(double));
+  for (double xi : pts)
+    for (double eta : pts) {
+      const double dx[4] = {2.0 * (-(1.0 - eta) / 4.0), 2.0 * ((1.0 - eta) / 4.0), 2.0 * ((1.0 + eta) / 4.0),
+                            2.0 * (-(1.0 + eta) / 4.0)};
+      const double dy[4] = {2.0 * (-(1.0 - xi) / 4.0), 2.0 * (-(1.0 + xi) / 4.0), 2.0 * ((1.0 + xi) / 4.0),
+                            2.0 * ((1.0 - xi) / 4.0)};
+      const double nv[4] = {(1.0 - xi) * (1.0 - eta) / 4.0, (1.0 + xi) * (1.0 - eta) / 4.0,
+                            (1.0 + xi) * (1.0 + eta) / 4.0, (1.0 - xi) * (1.0 + eta) / 4.0};
+      for (int i = 0; i < 4; ++i)
+        for (int j = i; j < 4; ++j) {
+          k16[i * 4 + j] += 0.25 * (dx[i] * dx[j] + dy[i] * dy[j]);
+          m16[i * 4 + j] += 0.25 * nv[i] * nv[j];
+        }
+    }
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < i; ++j) {
+      k16[i * 4 + j] = k16[j * 4 + i];
+      m16[i * 4 + j] = m16[j * 4 + i];
+    }
+}
+
+// The right-hand side of assemble_poisson (fem.cpp:243-276): the consistent
+// load -M f summed element by element (ex outer, ey inner), boundary entries
+// zeroed. node_source has (nx+1)(ny+1) entries in the reference node order.
+void tmg_inputs_poisson_rhs(int nx, int ny, const double* node_source, double* b) {
+  double k16[16], m16[16];
+  tmg_poisson_element_matrices(k16, m16);
+  const long n = static_cast<long>(nx + 1) * (ny + 1);
+  std::memset(b, 0, sizeof(double) * static_cast<size_t>(n));
+  for (int ex = 0; ex < nx; ++ex)
+    for (int ey = 0; ey < ny; ++ey) {
+      const long nd[4] = {static_cast<long>(ex) * (ny + 1) + ey, static_cast<long>(ex + 1) * (ny + 1) + ey,
+                          static_cast<long>(ex + 1) * (ny + 1) + ey + 1, static_cast<long>(ex) * (ny + 1) + ey + 1};
+      for (int a = 0; a < 4; ++a) {
+        double load = 0.0;
+        for (int c = 0; c < 4; ++c) load += m16[a * 4 + c] * node_source[nd[c]];
+        b[nd[a]] -= load;
+      }
+    }
+  for (int x = 0; x <= nx; ++x)
+    for (int y = 0; y <= ny; ++y)
+      if (x == 0 || y == 0 || x == nx || y == ny) b[static_cast<long>(x) * (ny + 1) + y] = 0.0;
+}
+
 }  // extern "C"

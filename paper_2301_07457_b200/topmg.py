@@ -552,6 +552,93 @@ def optimize(ops: MultigridOperators, material: MaterialModel, cfg: OptimConfig,
                        sec.value, bool(cv.value))
 
 
+# ------------------------------------------------------------- Poisson --
+# The paper's Poisson path (fem.cpp:232-276, bench.cpp:30-111; SURVEY.md 8(f)
+# item 3): 1 dof per node, every boundary node fixed.
+
+def poisson_element_matrices():
+    """(k_lap, m_mass), the 4x4 element matrices of fem.cpp:37-81."""
+    k, m = np.empty(16), np.empty(16)
+    _lib.load().tmg_poisson_element_matrices(dptr(k), dptr(m))
+    return k.reshape(4, 4), m.reshape(4, 4)
+
+
+def assemble_poisson_rhs(grid: GridLevel, source) -> np.ndarray:
+    """The right-hand side of assemble_poisson for a per-node (or constant)
+    source: -M f assembled element by element, boundary entries 0."""
+    n = (grid.nx + 1) * (grid.ny + 1)
+    f = np.ascontiguousarray(np.broadcast_to(np.asarray(source, dtype=np.float64), (n,)))
+    b = np.empty(n)
+    _lib.load().tmg_inputs_poisson_rhs(grid.nx, grid.ny, dptr(f), dptr(b))
+    return b
+
+
+def poisson_full_depth(grid: int) -> int:
+    """Coarsenings down to a 2x2 coarsest grid (bench.cpp:17-24)."""
+    d = 0
+    while grid > 2:
+        grid //= 2
+        d += 1
+    return d
+
+
+class PoissonMultigrid:
+    """build_hierarchy(nx, ny, nc, 1) + build_multigrid_operators of the
+    Poisson system, resident on the GPU."""
+
+    def __init__(self, grid: GridLevel, num_coarsenings: int, omega: float = 0.6, device: int = 0):
+        self.lib = _lib.load()
+        self.grid, self.nc = grid, num_coarsenings
+        h = C.c_void_p()
+        st = self.lib.tmg_poisson_create(grid.nx, grid.ny, num_coarsenings, device, C.byref(h))
+        if st:
+            _raise(st, "tmg_poisson_create: invalid hierarchy or CUDA failure")
+        self.h = h
+        self._check(self.lib.tmg_poisson_setup(self.h, omega))
+
+    def _check(self, st):
+        if st:
+            buf = C.create_string_buffer(512)
+            self.lib.tmg_poisson_last_error(self.h, buf, 512)
+            _raise(st, buf.value.decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.tmg_poisson_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def level_planes(self, level: int) -> np.ndarray:
+        """[5, (nx_l+1)(ny_l+1)]: centre, N, SE, E, NE stencil entries per node."""
+        nx, ny = self.grid.nx >> (self.nc - level), self.grid.ny >> (self.nc - level)
+        out = np.empty((5, (nx + 1) * (ny + 1)))
+        self._check(self.lib.tmg_poisson_level_values(self.h, level, dptr(out)))
+        return out
+
+    def vcycle(self, u: np.ndarray, f: np.ndarray, gamma: int = 1, pre: int = 2, post: int = 2) -> np.ndarray:
+        out = np.array(u, dtype=np.float64, copy=True)
+        ff = np.ascontiguousarray(f, dtype=np.float64)
+        self._check(self.lib.tmg_poisson_vcycle(self.h, dptr(ff), dptr(out), gamma, pre, post))
+        return out
+
+    def solve(self, b: np.ndarray, cfg: SolverConfig, x0: np.ndarray | None = None) -> SolveReport:
+        bb = np.ascontiguousarray(b, dtype=np.float64)
+        x0c = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+        x = np.empty_like(bb)
+        hist = np.empty(cfg.max_iter + 1)
+        it, cv, hl = C.c_int(), C.c_int(), C.c_int()
+        fr, sec = C.c_double(), C.c_double()
+        self._check(self.lib.tmg_poisson_solve(self.h, dptr(bb), dptr(x0c), cfg.tol, cfg.max_iter, cfg.gamma,
+                                               cfg.pre_sweeps, cfg.post_sweeps, dptr(x), C.byref(it), C.byref(fr),
+                                               C.byref(cv), C.byref(sec), dptr(hist), hist.size, C.byref(hl)))
+        return SolveReport(x, it.value, fr.value, bool(cv.value), sec.value, list(hist[: hl.value]))
+
+
 # ------------------------------------------------------------- outputs --
 # Byte-compatible with the reference writers (report.cpp:34-97, 153-168);
 # host-side, like the reference's (SURVEY.md 8(f) item 4).
