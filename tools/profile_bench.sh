@@ -1,3 +1,8 @@
+# The round's measurement set (run under gpurun from the repo root): the
+# default bench.py line, the reference arm, the ncu launch list of a short
+# bench run (after the same command exited 0 without ncu) and an
+# `ncu --set full` capture of the c4 fine and coarse passes.
+#   python tools/ncu_summary.py gpurun_out/full_r01.ncu-rep profiles/rNN/ncu.csv profiles/ncu_traffic.json
 set -x
 python bench.py > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo bench=$?
 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref=$?
