@@ -1,0 +1,114 @@
+"""Parity at BASELINE sizes (SURVEY.md 8(c) protocol), where the reference
+itself is too slow to run inside a test:
+
+c2 (2048^2, 16x16-element phase checkerboard, 1e9 contrast, 9 levels): the
+CPU checker (bit-exact to the reference) still assembles and builds the
+hierarchy here, so the device is compared against it directly: Galerkin
+levels, one V(2,2)-cycle, and the GPU solution's residual under the
+checker's assembled K.
+
+c4 (8192^2, 134M DOFs, 11 levels, the bench workload): size-independent
+properties only: the residual recomputed through a different kernel (the
+plain K.u pass) against the host right-hand side, compliance = b.u at
+convergence, bitwise run-to-run determinism and the symmetry of the
+preconditioner (test_solvers.cpp:387-409)."""
+import numpy as np
+import pytest
+
+import paper_2301_07457_b200 as P
+from helpers import MAT, moduli, rel
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c2():
+    nx = ny = 2048
+    nc = 8
+    _, E = moduli(nx, ny, "checker", 2)
+    g = P.GridLevel(nx, ny)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    ops = P.MultigridOperators(g, nc, 0.3, bc)
+    ops.set_moduli(E, 0.6)
+    sysc = po.System("orc", nx, ny, E, 0.3, bc.fixed_dofs, bc.point_loads).build_mg(nc, 0.6)
+    return ops, sysc, sysc.rhs(), nc
+
+
+def test_c2_galerkin_levels(c2):
+    ops, sysc, _, nc = c2
+    for lvl in (nc - 1, nc - 4, 1):
+        off, col, val = sysc.csr(lvl)
+        dval = ops.level_values(lvl, off, col)
+        assert np.max(np.abs(dval - val)) <= 1e-13 * np.max(np.abs(val)), lvl
+
+
+def test_c2_one_vcycle(c2):
+    ops, sysc, _, _ = c2
+    f = np.random.default_rng(2).standard_normal(sysc.n)
+    got = P.mg_cycle(ops, np.zeros_like(f), f, 1, 2, 2)
+    want = sysc.vcycle(f, np.zeros_like(f), 1, 2, 2)
+    # 1e9 contrast: the symmetric 8-value Ke (<= 1 ulp per entry, DESIGN.md
+    # 2) is amplified through the void phase; the reference's own
+    # reassociation moves a cycle by the same order
+    assert rel(got, want) <= 1e-10
+
+
+def test_c2_solution_residual_under_reference_K(c2):
+    """SURVEY.md 8(c) protocol for the 1e9-contrast configs. Plain CG's
+    recursively updated residual drifts from the true one at this contrast:
+    the reference's own tol-1e-8 solutions have true residuals of 2e-6 -
+    6e-6 under its own K (measured at 256^2 - 1024^2 with this recipe), and
+    the iteration count at which the recursive residual crosses 1e-8 is
+    chaotic (reported, not gated). Gated: the device solution's true residual
+    under the checker's assembled K is at that attainable level and equals
+    its true residual under the device operator to 1 %: the two operators
+    agree on the solution."""
+    ops, sysc, b, nc = c2
+    rep = P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-8, max_iter=2000, num_coarsenings=nc))
+    assert rep.converged
+    nb = np.linalg.norm(b)
+    r_ref = np.linalg.norm(b - sysc.matvec(nc, rep.solution)) / nb
+    r_dev = np.linalg.norm(b - ops.apply(nc, rep.solution)) / nb
+    assert r_ref <= 1e-5
+    assert abs(r_ref - r_dev) <= 0.01 * r_ref
+
+
+@pytest.fixture(scope="module")
+def c4():
+    nx = ny = 8192
+    nc = 10
+    g = P.GridLevel(nx, ny)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    E = P.effective_moduli(P.density_iid(nx, ny, 1), MAT)
+    ops = P.MultigridOperators(g, nc, 0.3, bc)
+    ops.set_moduli(E, 0.6)
+    return ops, P.assemble_rhs(g, bc), nc
+
+
+def test_c4_residual_compliance_determinism(c4):
+    ops, b, nc = c4
+    cfg = P.SolverConfig(tol=1e-8, max_iter=500, num_coarsenings=nc)
+    rep = P.pcgmg_solve(ops, b, cfg)
+    assert rep.converged and rep.iterations == 21  # the bench workload's count (BASELINE recipe)
+    u = rep.solution
+    # residual through the plain K.u pass (not the fused PCG kernels)
+    r = b - ops.apply(nc, u)
+    assert np.linalg.norm(r) / np.linalg.norm(b) <= 1e-8 * 1.001
+    # compliance u^T K u equals b^T u up to u^T r
+    c = P.compliance(ops)
+    bu = float(b @ u)
+    assert abs(c - bu) <= abs(float(u @ r)) + 1e-12 * abs(bu)
+    again = P.pcgmg_solve(ops, b, cfg)
+    assert again.iterations == rep.iterations and np.array_equal(again.solution, u)
+
+
+def test_c4_preconditioner_symmetric(c4):
+    ops, b, _ = c4
+    rng = np.random.default_rng(4)
+    x, y = rng.standard_normal(b.size), rng.standard_normal(b.size)
+    zero = np.zeros_like(b)
+    mx = P.mg_cycle(ops, zero, x, 1, 2, 2)
+    my = P.mg_cycle(ops, zero, y, 1, 2, 2)
+    lhs, rhs = float(y @ mx), float(x @ my)
+    assert abs(lhs - rhs) <= 1e-10 * max(abs(lhs), abs(rhs))
