@@ -505,18 +505,6 @@ __global__ void __launch_bounds__(kRedThreads) k_dot(const double2* __restrict__
   finish_reduction<kRedThreads>(s, partials, ticket, gridDim.x, op, st, hm, out);
 }
 
-// p = z + beta p (solvers.cpp:367-371); beta = 0 on the first iteration.
-__global__ void __launch_bounds__(kRedThreads) k_update_p(const double2* __restrict__ z,
-                                                          double2* __restrict__ p, long n2,
-                                                          const PcgState* st) {
-  const double beta = st->beta;
-  for (long k = blockIdx.x * static_cast<long>(kRedThreads) + threadIdx.x; k < n2;
-       k += static_cast<long>(gridDim.x) * kRedThreads) {
-    const double2 zz = z[k], pp = p[k];
-    p[k] = make_double2(zz.x + beta * pp.x, zz.y + beta * pp.y);
-  }
-}
-
 // x += alpha p; r -= alpha Ap; rr = r.r (solvers.cpp:383-386)
 __global__ void __launch_bounds__(kRedThreads) k_update_xr(double2* __restrict__ x,
                                                            double2* __restrict__ r,
