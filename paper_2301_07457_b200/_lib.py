@@ -13,7 +13,9 @@ import pathlib
 import numpy as np
 
 PKG_DIR = pathlib.Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "libtmg_gpu.so"
+# TMG_LIB_PATH points the loader at another build of the same library (A/B
+# timing of kernel variants within one GPU session); the default is in-tree
+LIB_PATH = pathlib.Path(os.environ.get("TMG_LIB_PATH", PKG_DIR / "libtmg_gpu.so"))
 
 _D = C.POINTER(C.c_double)
 _I = C.POINTER(C.c_int)
