@@ -85,17 +85,27 @@ __device__ __forceinline__ void s_fwd(const SPlanes& p, int k, int j, double2 v,
   y1 = fma(p.at(k + 2, j), v.x, y1);
   y1 = fma(p.at(k + 3, j), v.y, y1);
 }
-__device__ __forceinline__ void s_bwd(const SPlanes& p, int k, int j, double2 v, double& y0, double& y1) {
+template <class PL>
+__device__ __forceinline__ void s_bwd(const PL& p, int k, int j, double2 v, double& y0, double& y1) {
   y0 = fma(p.at(k, j), v.x, y0);
   y0 = fma(p.at(k + 2, j), v.y, y0);
   y1 = fma(p.at(k + 1, j), v.x, y1);
   y1 = fma(p.at(k + 3, j), v.y, y1);
 }
 
+// Stage B's left-column blocks held in registers: planes 7-18 of the left
+// column at rows j+1 (7-10), j (11-14) and j-1 (15-18), the only ones
+// s_apply reads through its L accessor
+struct LCache {
+  const double* v;
+  __device__ __forceinline__ double at(int k, int) const { return v[k - 7]; }
+};
+
 // Three independent accumulator pairs (centre/N/SE, E/NE/S, NW/W/SW) keep
 // three FMA chains in flight per thread; with two resident CTAs a single
 // chain per dof left the FP64 pipe waiting on its own latency.
-__device__ __forceinline__ void s_apply(const SPlanes& C, const SPlanes& L, int j, const double2 (&l)[3],
+template <class LP>
+__device__ __forceinline__ void s_apply(const SPlanes& C, const LP& L, int j, const double2 (&l)[3],
                                         const double2 (&c)[3], const double2 (&r)[3], double2& y, double2& d) {
   const double c00 = C.at(0, j), c01 = C.at(1, j), c11 = C.at(2, j);
   double a0 = c00 * c[1].x, a1 = c01 * c[1].x;
@@ -119,10 +129,10 @@ __device__ __forceinline__ void s_consumer_sync() {
   asm volatile("bar.sync 2, %0;" ::"n"(kSY) : "memory");
 }
 
-// rcp_nr from tmg_march.cuh; one reciprocal per component (coarse diagonals
-// differ between the two dofs)
-__device__ __forceinline__ double2 s_jacobi(double2 x, double2 f, double2 y, double2 d, double omega) {
-  return make_double2(fma(omega * rcp_nr(d.x), f.x - y.x, x.x), fma(omega * rcp_nr(d.y), f.y - y.y, x.y));
+// one damped-Jacobi update from the reciprocal diagonal (rcp_nr from
+// tmg_march.cuh, one per component: coarse diagonals differ between the dofs)
+__device__ __forceinline__ double2 s_jacobi_r(double2 x, double2 f, double2 y, double2 r, double omega) {
+  return make_double2(fma(omega * r.x, f.x - y.x, x.x), fma(omega * r.y, f.y - y.y, x.y));
 }
 
 template <bool UP>
@@ -132,9 +142,9 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
   __shared__ uint64_t full[kSStages], empty[kSStages];
   // row-exchange columns; one buffer each suffices: between a step's reads
   // of a buffer and the next step's writes to it lies a consumer barrier
-  __shared__ double2 xa[kSY + 2];  // stage-A inputs (x1 / w)
-  __shared__ double2 xb[kSY + 2];  // stage-B inputs (x2 / x3)
-  __shared__ double2 rb[kSY];      // DOWN: residual rows for the restriction
+  __shared__ double2 xa[kSY + 2];  // stage-A inputs (x1 / w), written in H1
+  __shared__ double2 xb[kSY + 2];  // stage-A outputs (x2 / x3), written in H2
+  __shared__ double2 rb[kSY];      // DOWN: stage-B residual rows, written in H2
   constexpr int kSlot = UP ? kSSlotUp : kSSlotDown;
 
   const Grid& g = a.g;
@@ -170,6 +180,10 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
       mbar_init(&empty[s], kSWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = t; i < kSY + 2; i += kSThreads) {
+    xa[i] = xb[i] = make_double2(0.0, 0.0);
+    if (i < kSY) rb[i] = make_double2(0.0, 0.0);
   }
   __syncthreads();
 
@@ -213,67 +227,87 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
   }
 
   // ------------------------------------------------------------ consumers
+  // Schedule per ring entry e (column c = cf + e), two consumer barriers:
+  //   H1: stage-A inputs of column c (-> xa); the stage-A column c-2 from xb
+  //       into the stage-B window; DOWN: restriction of the stage-B rows of
+  //       column c-4 (rb)
+  //   --- barrier ---
+  //   H2: stage A at column c-1 (-> xb) and stage B at column c-3 (-> out /
+  //       rb): independent, so their FMA chains interleave
+  //   --- barrier ---
+  // Stage B reads the transposed blocks of its left column from registers
+  // (cached when that column was its centre), so the ring still holds four
+  // columns (c-3 .. c). Nodes outside the level are masked by selects, not
+  // branches: the stencil is zero there (S is zero-filled and only level
+  // nodes are assembled), so the unmasked arithmetic is finite and discarded.
   const int yt = y0 + R0 + t;
   const int lane = t & 31;
   const int j = t + 1;  // stream row index of yt (streams start at yt - 1 for t = 0)
-  auto inside = [&](int x, int y) { return g.x0 + x >= 0 && g.x0 + x <= g.nx && y >= 0 && y <= g.ny; };
+  // halo stream row of the stage-A inputs this thread also computes (only
+  // threads 0 and kSY-1 store it; the rest compute it to stay convergent)
+  const int jh = (t == 0) ? 0 : kSY + 1;
+  const int yh = y0 + r0 + jh;
+  auto row_in = [&](int y) { return y >= 0 && y <= g.ny; };
+  auto col_in = [&](int x) { return g.x0 + x >= 0 && g.x0 + x <= g.nx; };
+  const bool rin = row_in(yt), hin = row_in(yh);
+  const bool tB = t >= 1 && t < kSY - 1;  // rows of stage B
   auto fat = [&](const unsigned char* s, int jj) {
     return *reinterpret_cast<const double2*>(s + kSO_F + misF + jj * 16);
   };
-  double2 acc = make_double2(0.0, 0.0);
-  // stage-A input at stream row jj of column c (slot s, previous slot ps)
-  auto a_in = [&](const unsigned char* s, const unsigned char* ps, int c, int jj, double2 xv) -> double2 {
+  const double2 z2 = make_double2(0.0, 0.0);
+  auto sel = [](bool p, double2 v) { return p ? v : make_double2(0.0, 0.0); };
+  // DOWN stage-A input: x1 = omega f / D (sweep 1 from zero); rc = 1/D
+  auto a_in_down = [&](const unsigned char* s, int jj, double2& rc) {
+    const SPlanes P{s, misS};
+    const double2 f = fat(s, jj);
+    rc = make_double2(rcp_nr(P.at(0, jj)), rcp_nr(P.at(2, jj)));
+    return make_double2(a.omega * f.x * rc.x, a.omega * f.y * rc.y);
+  };
+  // UP stage-A input: w = x2 + P u_c (bilinear, grid.cpp:20-46); coarse
+  // column ceil(c/2) in s, floor(c/2) in ps for odd columns
+  auto a_in_up = [&](const unsigned char* s, const unsigned char* ps, bool odd_col, int jj, double2 xv) {
     const int y = y0 + r0 + jj;
-    if (!inside(c, y)) return make_double2(0.0, 0.0);
-    if (!UP) {
-      const SPlanes P{s, misS};
-      const double2 f = fat(s, jj);
-      return make_double2(a.omega * f.x * rcp_nr(P.at(0, jj)), a.omega * f.y * rcp_nr(P.at(2, jj)));
-    }
-    // w = x2 + P u_c (bilinear, grid.cpp:20-46); coarse column ceil(c/2) in s,
-    // floor(c/2) in ps for odd columns; coarse row index of fine row y
     const int gy = y - 2 * ((y0 >> 1) + cr0);  // fine row relative to the coarse stream start
     auto crow = [&](const unsigned char* sl, int k) {
       return *reinterpret_cast<const double2*>(sl + kSO_C + misC + k * 16);
     };
     auto colv = [&](const unsigned char* sl) {
-      if (gy & 1) {
-        const double2 p = crow(sl, gy >> 1), q = crow(sl, (gy >> 1) + 1);
-        return make_double2(0.5 * p.x + 0.5 * q.x, 0.5 * p.y + 0.5 * q.y);
-      }
-      return crow(sl, gy >> 1);
+      const double2 p = crow(sl, gy >> 1), q = crow(sl, (gy >> 1) + 1);
+      return (gy & 1) ? make_double2(0.5 * p.x + 0.5 * q.x, 0.5 * p.y + 0.5 * q.y) : p;
     };
     double2 pu = colv(s);
-    if ((g.x0 + c) & 1) {
-      const double2 q = ps ? colv(ps) : make_double2(0.0, 0.0);
+    if (odd_col) {
+      const double2 q = colv(ps);
       pu = make_double2(0.5 * q.x + 0.5 * pu.x, 0.5 * q.y + 0.5 * pu.y);
     }
     return make_double2(xv.x + pu.x, xv.y + pu.y);
   };
 
-  // UP: x2 of the own row (and of the halo row of threads 0 / kSY-1) for
-  // the next column, loaded while the current one is processed
-  double2 x2o = make_double2(0.0, 0.0), x2h = make_double2(0.0, 0.0);
+  // UP: x2 of the own row and of the halo row for the next column, loaded
+  // while the current one is processed
+  double2 x2o = z2, x2h = z2;
   auto fetch_x2 = [&](int c) {
-    const int yo = y0 + r0 + j;
-    x2o = inside(c, yo) ? a.x2[g.idx(c, yo)] : make_double2(0.0, 0.0);
-    if (t == 0 || t == kSY - 1) {
-      const int yh = y0 + r0 + (t == 0 ? 0 : kSY + 1);
-      x2h = inside(c, yh) ? a.x2[g.idx(c, yh)] : make_double2(0.0, 0.0);
-    }
+    x2o = a.x2[g.idx(c, yt)];
+    x2h = a.x2[g.idx(c, yh)];
   };
   if (UP) fetch_x2(cf);
 
-  // rotating windows: A over stage-A inputs, B over stage-B inputs. The
-  // entry loop is unrolled by 3 so the windows (and the smem exchange
-  // buffers) rotate by compile-time index instead of register moves: at
-  // phase P the window columns x-1 / x / x+1 are w[P] / w[P+1] / w[P+2]
-  // (mod 3), w[P+2] being the column entered this step.
+  // rotating windows: A over stage-A inputs (columns c-2, c-1, c), B over
+  // stage-A outputs (c-4, c-3, c-2). The entry loop is unrolled by 3 so the
+  // windows rotate by compile-time index: at phase P the window columns are
+  // w[P], w[P+1], w[P+2] (mod 3), w[P+2] being the column read this step.
   double2 wa[3][3], wb[3][3];
+  double2 rd[3];  // DOWN: 1/D of the own row at the stage-A window columns
 #pragma unroll
-  for (int p = 0; p < 3; ++p)
+  for (int p = 0; p < 3; ++p) {
+    rd[p] = z2;
 #pragma unroll
-    for (int q = 0; q < 3; ++q) wa[p][q] = wb[p][q] = make_double2(0.0, 0.0);
+    for (int q = 0; q < 3; ++q) wa[p][q] = wb[p][q] = z2;
+  }
+  double lc[12];  // stage B: planes 7-10 at j+1, 11-14 at j, 15-18 at j-1 of its left column
+#pragma unroll
+  for (int k = 0; k < 12; ++k) lc[k] = 0.0;
+  double2 acc = z2, bres = z2;  // DOWN: restriction accumulator, own stage-B residual
 
   // ring position of entry e (slot index, mbarrier phase) and the slots of
   // entries e-1 .. e-3, advanced incrementally
@@ -288,82 +322,100 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
     constexpr int P = decltype(phase)::value;
     constexpr int IL = P, IC = (P + 1) % 3, IR = (P + 2) % 3;
     const int c = cf + e;
-    mbar_wait(&full[si], ph);
+    const bool enter = e < nent;
     const unsigned char* s0 = smem_raw + static_cast<size_t>(si) * kSlot;
-    const bool have0 = in_storage(c);
-    const unsigned char* s1 = (e >= 1 && in_storage(c - 1)) ? sp1 : nullptr;
-    const unsigned char* s2 = (e >= 2 && in_storage(c - 2)) ? sp2 : nullptr;
-    const unsigned char* s3 = (e >= 3 && in_storage(c - 3)) ? sp3 : nullptr;
-    // (1) stage-A inputs of column c
-    {
-      double2* buf = xa;
-      const double2 xo = x2o, xh = x2h;
-      if (UP && e + 1 < nent) fetch_x2(c + 1);
-      buf[t + 1] = have0 ? a_in(s0, s1, c, j, xo) : make_double2(0.0, 0.0);
-      if (t == 0) buf[0] = have0 ? a_in(s0, s1, c, 0, xh) : make_double2(0.0, 0.0);
-      if (t == kSY - 1) buf[kSY + 1] = have0 ? a_in(s0, s1, c, kSY + 1, xh) : make_double2(0.0, 0.0);
-      s_consumer_sync();
-#pragma unroll
-      for (int q = 0; q < 3; ++q) wa[IR][q] = buf[t + q];
-    }
-    // (2) stage A at column c-1
-    {
-      double2 v = make_double2(0.0, 0.0);
-      if (e >= 1 && s1 && s2 && inside(c - 1, yt)) {
-        double2 y, d;
-        s_apply(SPlanes{s1, misS}, SPlanes{s2, misS}, j, wa[IL], wa[IC], wa[IR], y, d);
-        v = s_jacobi(wa[IC][1], fat(s1, j), y, d, a.omega);
-        // x2 of the nodes this CTA owns: rows [y0, y0+kOwned), fine columns
-        // [2 X0, 2 X1) of its coarse columns
-        if (!UP && t >= 2 && t < 2 + kOwned && c - 1 > xlo && c - 1 <= xhi && c - 1 < g.ncol && yt <= g.ny)
-          a.out[g.idx(c - 1, yt)] = v;
+    // ---------------------------------------------------------------- H1
+    if (enter) {
+      mbar_wait(&full[si], ph);
+      const bool ci = col_in(c);
+      double2 v, vh;
+      if (!UP) {
+        double2 rc, rch;
+        v = a_in_down(s0, j, rc);
+        vh = a_in_down(s0, jh, rch);
+        rd[IR] = rc;
+      } else {
+        const bool odd = (g.x0 + c) & 1;
+        const double2 xo = x2o, xh = x2h;
+        if (e + 1 < nent) fetch_x2(c + 1);
+        v = a_in_up(s0, sp1, odd, j, xo);
+        vh = a_in_up(s0, sp1, odd, jh, xh);
       }
-      double2* buf = xb;
-      buf[t + 1] = v;
-      s_consumer_sync();
-#pragma unroll
-      for (int q = 0; q < 3; ++q) wb[IR][q] = (t >= 1 && t < kSY - 1) ? buf[t + q] : make_double2(0.0, 0.0);
+      xa[t + 1] = sel(ci && rin, v);
+      if (t == 0) xa[0] = sel(ci && hin, vh);
+      if (t == kSY - 1) xa[kSY + 1] = sel(ci && hin, vh);
     }
-    // (3) stage B at column c-2
-    if (e >= 2) {
-      const int x = c - 2;
-      double2 out = make_double2(0.0, 0.0);
-      if (t >= 1 && t < kSY - 1 && s2 && s3 && inside(x, yt)) {
-        double2 y, d;
-        s_apply(SPlanes{s2, misS}, SPlanes{s3, misS}, j, wb[IL], wb[IC], wb[IR], y, d);
-        const double2 f = fat(s2, j);
-        out = UP ? s_jacobi(wb[IC][1], f, y, d, a.omega) : make_double2(f.x - y.x, f.y - y.y);
-      }
-      if (UP) {
-        if (t >= 1 && t < kSY - 1 && x >= xlo && x <= xhi && yt <= g.ny) a.out[g.idx(x, yt)] = out;
-      } else if (x >= xlo && x <= xhi) {
-        // restriction: rows (1/2, 1, 1/2) around even fine rows, columns the same
-        double2* buf = rb;
-        buf[t] = out;
-        s_consumer_sync();
-        if ((yt & 1) == 0 && t >= 2 && t < kSY - 2) {
-          const double2 rm = buf[t - 1], rp = buf[t + 1];
-          const double2 rs = make_double2(fma(0.5, rm.x + rp.x, out.x), fma(0.5, rm.y + rp.y, out.y));
-          if (((g.x0 + x) & 1) == 0) {
-            acc.x += rs.x;
-            acc.y += rs.y;
-          } else {
-            if (x != xlo) {
-              acc.x = fma(0.5, rs.x, acc.x);
-              acc.y = fma(0.5, rs.y, acc.y);
-              const int X = (x - 1) >> 1, Y = yt >> 1;
-              if (yt >= y0 && yt < y0 + kOwned && Y <= a.gc.ny) a.fc[a.gc.idx(X, Y)] = make_double2(0.25 * acc.x, 0.25 * acc.y);
-            }
-            acc = make_double2(0.5 * rs.x, 0.5 * rs.y);
+    // stage-B window column c-2 (stage A ran there last step)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) wb[IR][q] = tB ? xb[t + q] : z2;
+    if (!UP && e >= 4) {
+      // restriction of column x = c-4: rows (1/2, 1, 1/2) around even fine
+      // rows, columns the same
+      const int x = c - 4;
+      if (x >= xlo && x <= xhi) {
+        const double2 rm = rb[t > 0 ? t - 1 : 0], rp = rb[t < kSY - 1 ? t + 1 : kSY - 1];
+        const double2 rs = make_double2(fma(0.5, rm.x + rp.x, bres.x), fma(0.5, rm.y + rp.y, bres.y));
+        if (((g.x0 + x) & 1) == 0) {
+          acc.x += rs.x;
+          acc.y += rs.y;
+        } else {
+          if (x != xlo) {
+            acc.x = fma(0.5, rs.x, acc.x);
+            acc.y = fma(0.5, rs.y, acc.y);
+            const int X = (x - 1) >> 1, Y = yt >> 1;
+            if ((yt & 1) == 0 && t >= 2 && t < kSY - 2 && yt >= y0 && yt < y0 + kOwned && Y <= a.gc.ny)
+              a.fc[a.gc.idx(X, Y)] = make_double2(0.25 * acc.x, 0.25 * acc.y);
           }
+          acc = make_double2(0.5 * rs.x, 0.5 * rs.y);
         }
       }
     }
-    // (4) column c-3 is no longer needed
-    if (e >= 3) {
+    s_consumer_sync();
+    // ---------------------------------------------------------------- H2
+    if (enter) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) wa[IR][q] = xa[t + q];
+    }
+    const bool runA = enter && e >= 2, runB = e >= 3 && e <= nent;
+    double2 va = z2, vb = z2;
+    double2 ya, da, yb, db;
+    if (runA) s_apply(SPlanes{sp1, misS}, SPlanes{sp2, misS}, j, wa[IL], wa[IC], wa[IR], ya, da);
+    if (runB) s_apply(SPlanes{sp3, misS}, LCache{lc}, j, wb[IL], wb[IC], wb[IR], yb, db);
+    if (runA) {
+      const int x = c - 1;
+      const double2 f = fat(sp1, j);
+      const double2 r = UP ? make_double2(rcp_nr(da.x), rcp_nr(da.y)) : rd[IC];
+      va = sel(col_in(x) && rin, s_jacobi_r(wa[IC][1], f, ya, r, a.omega));
+      // x2 of the nodes this CTA owns: rows [y0, y0+kOwned), fine columns
+      // [2 X0, 2 X1) of its coarse columns
+      if (!UP && t >= 2 && t < 2 + kOwned && x > xlo && x <= xhi && x < g.ncol && yt <= g.ny)
+        a.out[g.idx(x, yt)] = va;
+      xb[t + 1] = va;
+    }
+    if (runB) {
+      const int x = c - 3;
+      const SPlanes C{sp3, misS};
+      const double2 f = fat(sp3, j);
+      const bool ok = tB && col_in(x) && rin;
+      if (UP) {
+        vb = sel(ok, s_jacobi_r(wb[IC][1], f, yb, make_double2(rcp_nr(db.x), rcp_nr(db.y)), a.omega));
+        if (tB && x >= xlo && x <= xhi && yt <= g.ny) a.out[g.idx(x, yt)] = vb;
+      } else {
+        bres = sel(ok, make_double2(f.x - yb.x, f.y - yb.y));
+        rb[t] = bres;
+      }
+      // the transposed blocks of column x for stage B at x+1
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        lc[k] = C.at(7 + k, j + 1);
+        lc[4 + k] = C.at(11 + k, j);
+        lc[8 + k] = C.at(15 + k, j - 1);
+      }
+      // column c-3 is no longer needed
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[srel]);
     }
+    s_consumer_sync();
     // advance the ring position
     sp3 = sp2;
     sp2 = sp1;
@@ -375,14 +427,17 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
     }
   };
 
+  // entries 0 .. nent-1 plus drain steps: stage B trails the last entry by
+  // one step, the DOWN restriction by two
+  const int nsteps = nent + (UP ? 1 : 2);
   int e = 0;
-  for (; e + 2 < nent; e += 3) {
+  for (; e + 2 < nsteps; e += 3) {
     step(std::integral_constant<int, 0>{}, e);
     step(std::integral_constant<int, 1>{}, e + 1);
     step(std::integral_constant<int, 2>{}, e + 2);
   }
-  if (e < nent) step(std::integral_constant<int, 0>{}, e);
-  if (e + 1 < nent) step(std::integral_constant<int, 1>{}, e + 1);
+  if (e < nsteps) step(std::integral_constant<int, 0>{}, e);
+  if (e + 1 < nsteps) step(std::integral_constant<int, 1>{}, e + 1);
 }
 
 }  // namespace tmg
