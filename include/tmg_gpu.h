@@ -72,11 +72,14 @@ void tmg_gpu_destroy(tmg_gpu_handle* h);
  * every rank and solved redundantly. replicated_level = -1 picks the finest
  * level at which a slab would hold fewer than 16 node columns. Slab
  * boundaries are multiples of 2^(num_coarsenings - replicated_level) fine
- * columns. The PCG scalars are summed over ranks in rank order. */
+ * columns and of the fine-level reduction tile width (8..64 columns, from
+ * nx and ny). Reductions sum per-tile partials of a global tile layout in one
+ * fixed order, so every partition (1..N ranks) gives bitwise the same PCG
+ * scalars, iterates and solution as the single-rank solve. */
 
 /* x0s[r] = first fine node column of rank r (nranks + 1 entries, the last is
  * nx + 1); *rep_out = the replicated level used. Host-only. */
-int tmg_partition(int nx, int num_coarsenings, int nranks, int replicated_level, int* x0s, int* rep_out);
+int tmg_partition(int nx, int ny, int num_coarsenings, int nranks, int replicated_level, int* x0s, int* rep_out);
 /* One process, `nslabs` ranks on one device: the decomposition run end to end
  * on a single GPU (halo exchange by device copies). */
 int tmg_gpu_create_local_slabs(int nx, int ny, int num_coarsenings, int dofs_per_node, int device, int nslabs,

@@ -35,7 +35,7 @@ class OptimConfigC(C.Structure):
 SIGNATURES = [
     ("tmg_gpu_create", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_H)]),
     ("tmg_gpu_destroy", None, [_H]),
-    ("tmg_partition", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _I, _I]),
+    ("tmg_partition", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _I, _I]),
     ("tmg_gpu_create_local_slabs", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                              C.POINTER(_H)]),
     ("tmg_gpu_create_nccl", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,

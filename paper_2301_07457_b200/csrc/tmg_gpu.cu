@@ -156,8 +156,10 @@ struct Rank {
   double2 *x = nullptr, *r = nullptr, *ap = nullptr, *b = nullptr, *x0 = nullptr;
   double2* r2 = nullptr;  // second residual buffer: the fused update alternates r / r2
   double2* pbuf[2] = {nullptr, nullptr};  // PCG directions (old / new alternate)
-  double* partials = nullptr;
+  double* partials = nullptr;  // fine-level reduction partials, global tile layout
+  double* gparts = nullptr;    // several ranks: the all-reduced partial array
   unsigned* ticket = nullptr;
+  unsigned* rticket = nullptr;  // ticket for reducing launches (null with several ranks)
   PcgState* st = nullptr;
   HostMirror* hm = nullptr;      // pinned, mapped
   HostMirror* hm_dev = nullptr;  // device alias of hm
@@ -195,8 +197,9 @@ struct Comm {
   virtual void gather_columns(std::vector<Rank*>& rs, int level, const std::function<void*(Rank&)>& field,
                               size_t esize, long plane_stride, int planes, const std::vector<int>& X0,
                               const std::vector<int>& ncol, cudaStream_t s) = 0;
-  // scal[1] of every rank summed into scal[2] of every rank (rank order)
-  virtual void allreduce(std::vector<Rank*>& rs, cudaStream_t s) = 0;
+  // partials[0 .. n) of every rank summed elementwise into gparts of every
+  // rank (each element has one non-zero contributor, so the sum is exact)
+  virtual void allreduce(std::vector<Rank*>& rs, int n, cudaStream_t s) = 0;
   virtual bool local() const = 0;
 };
 
@@ -210,8 +213,8 @@ struct LocalComm : Comm {
     std::vector<const double*> p(n);
     std::vector<double*> o(n);
     for (int i = 0; i < n; ++i) {
-      p[i] = rs[i]->scal + 1;
-      o[i] = rs[i]->scal + 2;
+      p[i] = rs[i]->partials;
+      o[i] = rs[i]->gparts;
     }
     CK(cudaMalloc(&d_parts, sizeof(double*) * n));
     CK(cudaMalloc(&d_outs, sizeof(double*) * n));
@@ -258,8 +261,8 @@ struct LocalComm : Comm {
       }
     }
   }
-  void allreduce(std::vector<Rank*>&, cudaStream_t s) override {
-    k_sum_ranks<<<1, 1, 0, s>>>(d_parts, n, d_outs);
+  void allreduce(std::vector<Rank*>&, int len, cudaStream_t s) override {
+    k_sum_parts<<<(len + 255) / 256, 256, 0, s>>>(d_parts, n, d_outs, len);
     CKL();
   }
 };
@@ -309,8 +312,8 @@ struct NcclComm : Comm {
       }
     NK(nccl().groupEnd());
   }
-  void allreduce(std::vector<Rank*>& rs, cudaStream_t s) override {
-    NK(nccl().allReduce(rs[0]->scal + 1, rs[0]->scal + 2, 1, ncclDouble, ncclSum, comm, s));
+  void allreduce(std::vector<Rank*>& rs, int len, cudaStream_t s) override {
+    NK(nccl().allReduce(rs[0]->partials, rs[0]->gparts, len, ncclDouble, ncclSum, comm, s));
   }
 };
 
@@ -339,6 +342,8 @@ struct tmg_gpu_handle {
   long graph_kernels[3] = {0, 0, 0};
   int g_gamma = -1, g_pre = -1, g_post = -1;
   bool g_fused = false;
+  // node columns per tile of the fine-level reductions (red_tiles)
+  int red_tx = 64;
   // coarse levels at least this large use the two-stage kernels
   // (TMG_SMARCH_MIN_NODES overrides it, for tests on small meshes)
   long smarch_min_nodes = kSMinNodes;
@@ -368,11 +373,27 @@ using H = tmg_gpu_handle;
 
 // ------------------------------------------------------------- geometry ----
 
-// Fine node-column partition: boundaries multiples of 2^(nc - rep) so every
-// distributed level has even slab boundaries.
-std::vector<int> partition(int nx, int nc, int rep, int nranks) {
+// Node columns per tile of the fine-level reductions: the marching kernels'
+// strip width for the whole fine level (strip_tx below, the same formula),
+// rounded up to a power of two. It depends on the global mesh only, so every
+// partition tiles the fine level identically.
+int red_tx_of(int nx, int ny) {
+  const long rows_tiles = (ny + 1L + kRedRows - 1) / kRedRows;
+  const long want = ((nx + 1L) * rows_tiles + 148 * 8 - 1) / (148 * 8);
+  int tx = 8;
+  while (tx < 64 && tx < want) tx *= 2;
+  return tx;
+}
+
+// Fine node-column partition: boundaries multiples of 2^(nc - rep), so every
+// distributed level has even slab boundaries, and of the reduction tile
+// width, so no reduction tile straddles two ranks (both powers of two).
+int partition_gran(int nx, int ny, int nc, int rep) {
+  return std::max(1 << (nc - rep), red_tx_of(nx, ny));
+}
+std::vector<int> partition(int nx, int ny, int nc, int rep, int nranks) {
   std::vector<int> xp(nranks + 1, 0);
-  const long gran = 1L << (nc - rep);
+  const long gran = partition_gran(nx, ny, nc, rep);
   for (int r = 1; r < nranks; ++r) {
     const double target = static_cast<double>(r) * (nx + 1) / nranks;
     xp[r] = static_cast<int>(std::llround(target / gran) * gran);
@@ -464,7 +485,8 @@ void free_rank(Rank& R) {
                   static_cast<void*>(R.LiT), static_cast<void*>(R.Ainv), static_cast<void*>(R.bad_row),
                   static_cast<void*>(R.x), static_cast<void*>(R.r), static_cast<void*>(R.r2), static_cast<void*>(R.ap),
                   static_cast<void*>(R.b), static_cast<void*>(R.x0), static_cast<void*>(R.pbuf[0]),
-                  static_cast<void*>(R.pbuf[1]), static_cast<void*>(R.partials), static_cast<void*>(R.ticket),
+                  static_cast<void*>(R.pbuf[1]), static_cast<void*>(R.partials), static_cast<void*>(R.gparts),
+                  static_cast<void*>(R.ticket),
                   static_cast<void*>(R.st), static_cast<void*>(R.scal), static_cast<void*>(R.dense),
                   static_cast<void*>(R.aux), static_cast<void*>(R.aux2), static_cast<void*>(R.ocbuf)})
     cudaFree(p);
@@ -484,6 +506,16 @@ void free_handle(H* h) {
   for (cudaEvent_t e : h->uev)
     if (e) cudaEventDestroy(e);
   if (h->stream) cudaStreamDestroy(h->stream);
+}
+
+// tile geometry of the fine-level reductions on a rank's slab g
+RedTiles red_tiles(const H* h, const Grid& g) {
+  RedTiles rt{};
+  rt.tx = h->red_tx;
+  rt.ctile0 = g.x0 / h->red_tx;
+  const int ty = (h->ny + kRedRows) / kRedRows;  // ceil((ny + 1) / kRedRows)
+  rt.nparts = ty * ((h->nx + 1 + h->red_tx - 1) / h->red_tx);
+  return rt;
 }
 
 void alloc_rank(H* h, Rank& R) {
@@ -533,13 +565,18 @@ void alloc_rank(H* h, Rank& R) {
   CK(cudaMalloc(&R.Ainv, n0sq));
   CK(cudaMalloc(&R.bad_row, sizeof(int)));
   const dim3 ng = node_grid(F.g);
-  // one partial per CTA of any reducing launch: node grids and marching
-  // grids down to one column per CTA
-  const long march_ctas = (static_cast<long>(F.g.ny) / kTY + 2) * (F.g.ncol + 1);
-  const long nparts = std::max({static_cast<long>(ng.x) * ng.y, march_ctas, static_cast<long>(kRedBlocks)});
+  // reduction partials: the global tile array (zero outside this rank's
+  // tiles, which it never writes), or one per CTA of a node-grid launch
+  const long nparts = std::max(static_cast<long>(ng.x) * ng.y, static_cast<long>(red_tiles(h, F.g).nparts));
   CK(cudaMalloc(&R.partials, sizeof(double) * nparts));
+  CK(cudaMemsetAsync(R.partials, 0, sizeof(double) * nparts, s));
+  if (h->multi()) {
+    CK(cudaMalloc(&R.gparts, sizeof(double) * nparts));
+    CK(cudaMemsetAsync(R.gparts, 0, sizeof(double) * nparts, s));
+  }
   CK(cudaMalloc(&R.ticket, sizeof(unsigned)));
   CK(cudaMemsetAsync(R.ticket, 0, sizeof(unsigned), s));
+  R.rticket = h->multi() ? nullptr : R.ticket;
   CK(cudaMalloc(&R.st, sizeof(PcgState)));
   CK(cudaMemsetAsync(R.st, 0, sizeof(PcgState), s));
   CK(cudaMalloc(&R.scal, 4 * sizeof(double)));
@@ -568,17 +605,21 @@ void gather_level(H* h, int l, const std::function<void*(Rank&)>& field, size_t 
 // ---------------------------------------------------------- reductions ----
 
 // Launch a reduction on every rank: single rank -> the kernel's last block
-// applies `op`; several ranks -> partials, all-reduce, then k_scalar.
+// applies `op`; several ranks -> the kernels only write their tiles'
+// partials (rticket is null), the partial arrays are all-reduced and every
+// rank finishes the same array in the same fixed order (k_finish), so the
+// scalars are bitwise those of the single-rank solve.
 void reduce(H* h, RedOp op, const std::function<void(Rank&, RedOp, double*)>& launch, bool want_out = false) {
   if (!h->multi()) {
     Rank& R = *h->ranks[0];
     launch(R, op, want_out ? R.scal : nullptr);
     return;
   }
-  for (Rank* R : h->ranks) launch(*R, kRedPlain, R->scal + 1);
-  h->comm->allreduce(h->ranks, h->stream);
+  for (Rank* R : h->ranks) launch(*R, op, nullptr);
+  const int n = red_tiles(h, h->ranks[0]->fine().g).nparts;
+  h->comm->allreduce(h->ranks, n, h->stream);
   for (Rank* R : h->ranks) {
-    k_scalar<<<1, 1, 0, h->stream>>>(op, R->scal + 2, R->st, R->hm_dev, want_out ? R->scal : nullptr);
+    k_finish<<<1, 128, 0, h->stream>>>(R->gparts, n, op, R->st, R->hm_dev, want_out ? R->scal : nullptr);
     CKL();
   }
   h->count(static_cast<long>(h->ranks.size()) + (h->comm->local() ? 1 : 0));
@@ -642,7 +683,8 @@ MarchArgs march_args(H* h, Rank& R, const double2* u) {
   a.M = R.M;
   a.omega = h->omega;
   a.partials = R.partials;
-  a.ticket = R.ticket;
+  a.ticket = R.rticket;
+  a.rt = red_tiles(h, R.fine().g);
   a.rop = kRedNone;
   a.st = R.st;
   a.hm = R.hm_dev;
@@ -666,7 +708,8 @@ void launch_march(H* h, MarchArgs a) {
     grid = dim3(ty, (a.gc.ncol + a.tx - 1) / a.tx);
   } else {
     const long ty = (a.g.ny + 1 + Stage::kOwned - 1) / Stage::kOwned;
-    a.tx = strip_tx(ty, a.g.ncol);
+    // reducing stages march the reduction tiles (global geometry)
+    a.tx = RED ? h->red_tx : strip_tx(ty, a.g.ncol);
     grid = dim3(ty, (a.g.ncol + a.tx - 1) / a.tx);
   }
   k_march<Stage, RED><<<grid, kMarchThreads, sm, h->stream>>>(a);
@@ -868,7 +911,8 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
   }
   bool restricted = false;
   // the two-stage kernels pay off once a level streams more than it waits
-  const bool big = static_cast<long>(rs[0]->lev[l].g.ncol) * (rs[0]->lev[l].g.ny + 1) >= h->smarch_min_nodes;
+  // (decided on the global level size, so every partition runs the same kernels)
+  const bool big = (static_cast<long>(rs[0]->lev[l].g.nx) + 1) * (rs[0]->lev[l].g.ny + 1) >= h->smarch_min_nodes;
   if (!fine && big && zero && pre == 2) {
     // coarse level: both pre-sweeps, the residual and the restriction in one
     // pass over the stencil (tmg_smarch.cuh)
@@ -962,6 +1006,12 @@ int red_grid(long n2) {
   return static_cast<int>(b < kRedBlocks ? (b < 1 ? 1 : b) : kRedBlocks);
 }
 
+// launch grid of a fine-level reduction over a rank's slab: (row tiles,
+// local column tiles)
+dim3 red_launch_grid(const H* h, const Grid& g) {
+  return dim3((g.ny + kRedRows) / kRedRows, (g.ncol + h->red_tx - 1) / h->red_tx);
+}
+
 // a.b over the owned columns of the finest level of every rank
 void dot(H* h, const std::function<const double2*(Rank&)>& a, const std::function<const double2*(Rank&)>& b,
          RedOp op, bool want_out) {
@@ -969,9 +1019,8 @@ void dot(H* h, const std::function<const double2*(Rank&)>& a, const std::functio
       h, op,
       [&](Rank& R, RedOp rop, double* out) {
         const Grid& g = R.fine().g;
-        const long o = g.own_begin(), n2 = g.own_count();
-        k_dot<<<red_grid(n2), kRedThreads, 0, h->stream>>>(a(R) + o, b(R) + o, n2, R.partials, R.ticket, rop, R.st,
-                                                           R.hm_dev, out);
+        k_dot<<<red_launch_grid(h, g), kRedRows, 0, h->stream>>>(a(R), b(R), g, red_tiles(h, g), R.partials,
+                                                                 R.rticket, rop, R.st, R.hm_dev, out);
         CKL();
         h->count();
       },
@@ -1030,10 +1079,10 @@ void capture_iteration(H* h, int gamma, int pre, int post) {
       } else {
         // x += alpha p; r -= alpha Ap; rr (solvers.cpp:383-386)
         reduce(h, kRedRr, [&](Rank& R, RedOp rop, double* out) {
-          const long o = R.fine().g.own_begin(), no = R.fine().g.own_count();
-          k_update_xr<<<red_grid(no), kRedThreads, 0, h->stream>>>(R.x + o, R.r + o, R.pbuf[k ^ 1] + o,
-                                                                     R.ap + o, no, R.partials, R.ticket, rop, R.st,
-                                                                     R.hm_dev, out);
+          const Grid& g = R.fine().g;
+          k_update_xr<<<red_launch_grid(h, g), kRedRows, 0, h->stream>>>(R.x, R.r, R.pbuf[k ^ 1], R.ap, g,
+                                                                         red_tiles(h, g), R.partials, R.rticket,
+                                                                         rop, R.st, R.hm_dev, out);
           CKL();
           h->count();
         });
@@ -1067,9 +1116,10 @@ void capture_iteration(H* h, int gamma, int pre, int post) {
 void finish_update(H* h, int it) {
   const int k = (it - 1) & 1;
   reduce(h, kRedRr, [&](Rank& R, RedOp rop, double* out) {
-    const long o = R.fine().g.own_begin(), no = R.fine().g.own_count();
-    k_update_xr<<<red_grid(no), kRedThreads, 0, h->stream>>>(R.x + o, R.rbuf(k) + o, R.pbuf[k ^ 1] + o, R.ap + o,
-                                                               no, R.partials, R.ticket, rop, R.st, R.hm_dev, out);
+    const Grid& g = R.fine().g;
+    k_update_xr<<<red_launch_grid(h, g), kRedRows, 0, h->stream>>>(R.x, R.rbuf(k), R.pbuf[k ^ 1], R.ap, g,
+                                                                   red_tiles(h, g), R.partials, R.rticket, rop,
+                                                                   R.st, R.hm_dev, out);
     CKL();
     h->count();
   });
@@ -1339,12 +1389,13 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
   hp->ny = ny;
   hp->nc = nc;
   hp->nranks = nranks;
+  hp->red_tx = red_tx_of(nx, ny);
   hp->rep = (nranks == 1) ? nc : (rep >= 0 ? std::min(rep, nc - 1) : auto_rep(nx, nc, nranks));
   if (nranks > 1) {
     if (nc < 1 || hp->rep >= nc) return cfg("a distributed solve needs at least the finest level distributed");
-    hp->xpart = partition(nx, nc, hp->rep, nranks);
+    hp->xpart = partition(nx, ny, nc, hp->rep, nranks);
     for (int r = 0; r < nranks; ++r)
-      if (hp->xpart[r + 1] - hp->xpart[r] < (2 << (nc - hp->rep)))
+      if (hp->xpart[r + 1] - hp->xpart[r] < 2 * partition_gran(nx, ny, nc, hp->rep))
         return cfg("mesh too small for " + std::to_string(nranks) + " slabs");
   } else {
     hp->xpart = {0, nx + 1};
@@ -1437,12 +1488,13 @@ int tmg_nccl_unique_id(void* out128) {
   }
 }
 
-int tmg_partition(int nx, int num_coarsenings, int nranks, int replicated_level, int* x0s, int* rep_out) {
-  if (nranks < 1 || num_coarsenings < 0) return TMG_ERR_CONFIG;
+int tmg_partition(int nx, int ny, int num_coarsenings, int nranks, int replicated_level, int* x0s, int* rep_out) {
+  if (nranks < 1 || num_coarsenings < 0 || nx < 1 || ny < 1) return TMG_ERR_CONFIG;
   const int rep = nranks == 1 ? num_coarsenings
                               : (replicated_level >= 0 ? std::min(replicated_level, num_coarsenings - 1)
                                                        : auto_rep(nx, num_coarsenings, nranks));
-  const std::vector<int> xp = nranks == 1 ? std::vector<int>{0, nx + 1} : partition(nx, num_coarsenings, rep, nranks);
+  const std::vector<int> xp =
+      nranks == 1 ? std::vector<int>{0, nx + 1} : partition(nx, ny, num_coarsenings, rep, nranks);
   std::memcpy(x0s, xp.data(), sizeof(int) * xp.size());
   if (rep_out) *rep_out = rep;
   return TMG_OK;

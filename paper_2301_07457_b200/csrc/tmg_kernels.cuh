@@ -61,32 +61,63 @@ enum RedOp { kRedNone = 0, kRedZr = 1, kRedPap = 2, kRedRr = 3, kRedB = 4, kRedP
 
 __device__ __forceinline__ void apply_scalar(RedOp op, double acc, PcgState* st, HostMirror* hm, double* out);
 
-// Final stage: the last block to finish sums all partials in index order.
-// Deterministic for a fixed grid: the order never depends on which block
-// arrives last.
+// Fixed-order sum of p[0 .. n): exactly 128 lanes (the first four warps of
+// the block; blockDim >= 128) stride the array, then a fixed tree. The order
+// depends on n only, never on the launch that calls it, so the in-kernel
+// finish of a single-rank reduction and k_finish after a multi-rank
+// all-reduce of the same partial array give bitwise-equal sums. Valid in
+// every thread; every thread of the block must call it.
+__device__ __forceinline__ double fixed_sum(const double* p, int n) {
+  __shared__ double sh[4];
+  const int t = threadIdx.x + threadIdx.y * blockDim.x;
+  if (t < 128) {
+    double acc = 0.0;
+    for (int k = t; k < n; k += 128) acc += __ldcg(p + k);
+    acc = warp_sum(acc);
+    if ((t & 31) == 0) sh[t >> 5] = acc;
+  }
+  __syncthreads();
+  const double r = (sh[0] + sh[1]) + (sh[2] + sh[3]);
+  __syncthreads();
+  return r;
+}
+
+// Per-CTA partial into partials[pidx]; then, with a ticket (single rank), the
+// last CTA to finish sums all nparts partials in the fixed order and applies
+// `op`. Without a ticket (several ranks) the partials stay for the
+// all-reduce and k_finish. The partial index is a global tile index
+// (DESIGN.md section 5), so 1..N ranks produce the same partial array.
 template <int NT>
-__device__ __forceinline__ void finish_reduction(double part, double* partials,
-                                                 unsigned* ticket, int nblocks,
-                                                 RedOp op, PcgState* st,
+__device__ __forceinline__ void finish_reduction(double part, double* partials, int pidx, unsigned* ticket,
+                                                 int nlocal, int nparts, RedOp op, PcgState* st,
                                                  HostMirror* hm, double* out) {
   const int t = threadIdx.x + threadIdx.y * blockDim.x;
-  const int b = blockIdx.x + blockIdx.y * gridDim.x;
-  double s = block_sum<NT>(part);
+  const double s = block_sum<NT>(part);
   __shared__ bool last;
   if (t == 0) {
-    partials[b] = s;
-    __threadfence();
-    last = (atomicAdd(ticket, 1u) == static_cast<unsigned>(nblocks - 1));
+    partials[pidx] = s;
+    if (ticket) {
+      __threadfence();
+      last = (atomicAdd(ticket, 1u) == static_cast<unsigned>(nlocal - 1));
+    } else {
+      last = false;
+    }
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
-  double acc = 0.0;
-  for (int k = t; k < nblocks; k += NT) acc += __ldcg(partials + k);
-  acc = block_sum<NT>(acc);
+  const double acc = fixed_sum(partials, nparts);
   if (t != 0) return;
   *ticket = 0u;
   apply_scalar(op, acc, st, hm, out);
+}
+
+// one partial per CTA of the grid, in block order (single-rank launches)
+template <int NT>
+__device__ __forceinline__ void finish_reduction(double part, double* partials, unsigned* ticket, int nblocks,
+                                                 RedOp op, PcgState* st, HostMirror* hm, double* out) {
+  finish_reduction<NT>(part, partials, blockIdx.x + blockIdx.y * gridDim.x, ticket, nblocks, nblocks, op, st, hm,
+                       out);
 }
 
 // Scalar tail of a reduction: the global sum `acc` updates the PCG state
@@ -141,15 +172,21 @@ __device__ __forceinline__ void apply_scalar(RedOp op, double acc, PcgState* st,
   }
 }
 
-// Multi-rank reductions: every rank's partial sums to one global value in
-// rank order (deterministic), then the scalar tail runs on each rank's state.
-__global__ void k_scalar(RedOp op, const double* gsum, PcgState* st, HostMirror* hm, double* out) {
-  apply_scalar(op, *gsum, st, hm, out);
+// Multi-rank reductions: the ranks' partial arrays (each rank fills its own
+// tiles, zeros elsewhere) are summed elementwise, which is exact, then every
+// rank finishes the same array in the fixed order (one block of 128).
+__global__ void __launch_bounds__(128) k_finish(const double* parts, int n, RedOp op, PcgState* st,
+                                                HostMirror* hm, double* out) {
+  const double acc = fixed_sum(parts, n);
+  if (threadIdx.x == 0) apply_scalar(op, acc, st, hm, out);
 }
-__global__ void k_sum_ranks(const double* const* parts, int n, double* const* outs) {
+// in-process ranks: elementwise sum of the partial arrays in rank order
+__global__ void k_sum_parts(const double* const* parts, int nr, double* const* outs, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
   double s = 0.0;
-  for (int r = 0; r < n; ++r) s += *parts[r];
-  for (int r = 0; r < n; ++r) *outs[r] = s;
+  for (int r = 0; r < nr; ++r) s += parts[r][i];
+  for (int r = 0; r < nr; ++r) outs[r][i] = s;
 }
 
 // --------------------------------------------------------- node kernels --
@@ -491,44 +528,63 @@ __global__ void __launch_bounds__(kCoarseSolveThreads) k_coarse_solve(const doub
 // --------------------------------------------------- PCG vector ops (K8) --
 
 // Grid-stride dot over flat padded vectors (ghosts are 0 and add exactly 0).
-__global__ void __launch_bounds__(kRedThreads) k_dot(const double2* __restrict__ a,
-                                                     const double2* __restrict__ b, long n2,
-                                                     double* partials, unsigned* ticket, RedOp op,
-                                                     PcgState* st, HostMirror* hm, double* out) {
+// Tile geometry of the fine-level reductions: row tiles of kRedRows rows and
+// global column tiles of `tx` node columns (the marching kernels' tiles), so
+// a partial covers the same nodes, summed in the same order, whatever the
+// slab partition. Partial index = row tile + TY * global column tile.
+constexpr int kRedRows = 128;
+struct RedTiles {
+  int tx;      // node columns per tile
+  int ctile0;  // global column tile of local column 0 (g.x0 / tx)
+  int nparts;  // TY * global column tiles
+};
+
+// a.b over the owned nodes; thread = row, marching the tile's columns
+__global__ void __launch_bounds__(kRedRows) k_dot(const double2* __restrict__ a, const double2* __restrict__ b,
+                                                  Grid g, RedTiles rt, double* partials, unsigned* ticket,
+                                                  RedOp op, PcgState* st, HostMirror* hm, double* out) {
+  const int y = blockIdx.x * kRedRows + threadIdx.x;
+  const int xlo = blockIdx.y * rt.tx, xhi = min(xlo + rt.tx, g.ncol);
   double s = 0.0;
-  for (long k = blockIdx.x * static_cast<long>(kRedThreads) + threadIdx.x; k < n2;
-       k += static_cast<long>(gridDim.x) * kRedThreads) {
-    const double2 u = a[k], v = b[k];
-    s = fma(u.x, v.x, s);
-    s = fma(u.y, v.y, s);
+  if (y <= g.ny) {
+    for (int x = xlo; x < xhi; ++x) {
+      const long i = g.idx(x, y);
+      const double2 u = a[i], v = b[i];
+      s = fma(u.x, v.x, s);
+      s = fma(u.y, v.y, s);
+    }
   }
-  finish_reduction<kRedThreads>(s, partials, ticket, gridDim.x, op, st, hm, out);
+  finish_reduction<kRedRows>(s, partials, blockIdx.x + gridDim.x * (rt.ctile0 + blockIdx.y), ticket,
+                             gridDim.x * gridDim.y, rt.nparts, op, st, hm, out);
 }
 
 // x += alpha p; r -= alpha Ap; rr = r.r (solvers.cpp:383-386)
-__global__ void __launch_bounds__(kRedThreads) k_update_xr(double2* __restrict__ x,
-                                                           double2* __restrict__ r,
-                                                           const double2* __restrict__ p,
-                                                           const double2* __restrict__ ap, long n2,
-                                                           double* partials, unsigned* ticket,
-                                                           RedOp rop, PcgState* st, HostMirror* hm,
-                                                           double* out) {
+__global__ void __launch_bounds__(kRedRows) k_update_xr(double2* __restrict__ x, double2* __restrict__ r,
+                                                        const double2* __restrict__ p,
+                                                        const double2* __restrict__ ap, Grid g, RedTiles rt,
+                                                        double* partials, unsigned* ticket, RedOp rop,
+                                                        PcgState* st, HostMirror* hm, double* out) {
   const double alpha = st->alpha;
+  const int y = blockIdx.x * kRedRows + threadIdx.x;
+  const int xlo = blockIdx.y * rt.tx, xhi = min(xlo + rt.tx, g.ncol);
   double s = 0.0;
-  for (long k = blockIdx.x * static_cast<long>(kRedThreads) + threadIdx.x; k < n2;
-       k += static_cast<long>(gridDim.x) * kRedThreads) {
-    const double2 pp = p[k], aa = ap[k];
-    double2 xx = x[k], rr = r[k];
-    xx.x += alpha * pp.x;
-    xx.y += alpha * pp.y;
-    rr.x += -alpha * aa.x;
-    rr.y += -alpha * aa.y;
-    x[k] = xx;
-    r[k] = rr;
-    s = fma(rr.x, rr.x, s);
-    s = fma(rr.y, rr.y, s);
+  if (y <= g.ny) {
+    for (int xc = xlo; xc < xhi; ++xc) {
+      const long k = g.idx(xc, y);
+      const double2 pp = p[k], aa = ap[k];
+      double2 xx = x[k], rr = r[k];
+      xx.x += alpha * pp.x;
+      xx.y += alpha * pp.y;
+      rr.x += -alpha * aa.x;
+      rr.y += -alpha * aa.y;
+      x[k] = xx;
+      r[k] = rr;
+      s = fma(rr.x, rr.x, s);
+      s = fma(rr.y, rr.y, s);
+    }
   }
-  finish_reduction<kRedThreads>(s, partials, ticket, gridDim.x, rop, st, hm, out);
+  finish_reduction<kRedRows>(s, partials, blockIdx.x + gridDim.x * (rt.ctile0 + blockIdx.y), ticket,
+                             gridDim.x * gridDim.y, rt.nparts, rop, st, hm, out);
 }
 
 // r = b - t (t = A x0) ; plain copy when t == nullptr

@@ -102,7 +102,8 @@ struct MarchArgs {
   double2* out2;      // StSweep01U: x (read and written, own rows)
   double omega;
   double* partials;
-  unsigned* ticket;
+  unsigned* ticket;   // null: leave the partials for the multi-rank all-reduce
+  RedTiles rt;        // global tile geometry of the partials (reducing stages)
   RedOp rop;
   PcgState* st;
   HostMirror* hm;
@@ -738,9 +739,10 @@ __global__ void __launch_bounds__(kMarchThreads) k_march(MarchArgs a) {
       }
     }
   }
-  if (RED) {
-    finish_reduction<kMarchThreads>(part, a.partials, a.ticket, gridDim.x * gridDim.y, a.rop, a.st, a.hm,
-                                    a.red_out);
+  if constexpr (RED) {
+    static_assert(Stage::kOwned == kRedRows && Stage::kRow0 == 0, "reducing stages use the reduction tiles");
+    finish_reduction<kMarchThreads>(part, a.partials, blockIdx.x + gridDim.x * (a.rt.ctile0 + blockIdx.y), a.ticket,
+                                    gridDim.x * gridDim.y, a.rt.nparts, a.rop, a.st, a.hm, a.red_out);
   }
 }
 

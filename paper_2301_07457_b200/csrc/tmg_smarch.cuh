@@ -285,12 +285,18 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
 
   // UP: x2 of the own row and of the halo row for the next column, loaded
   // while the current one is processed
+  // (the column three entries further is prefetched into L2 at the same
+  // time: one step of lead alone left the warps waiting on HBM latency)
   double2 x2o = z2, x2h = z2;
   auto fetch_x2 = [&](int c) {
     x2o = a.x2[g.idx(c, yt)];
     x2h = a.x2[g.idx(c, yh)];
+    if (c + 3 <= cl) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.x2 + g.idx(c + 3, yt)));
   };
-  if (UP) fetch_x2(cf);
+  if (UP) {
+    for (int k = 1; k < 3; ++k) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.x2 + g.idx(cf + k, yt)));
+    fetch_x2(cf);
+  }
 
   // rotating windows: A over stage-A inputs (columns c-2, c-1, c), B over
   // stage-A outputs (c-4, c-3, c-2). The entry loop is unrolled by 3 so the

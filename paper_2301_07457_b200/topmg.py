@@ -364,11 +364,11 @@ class MultigridOperators:
         return s.value, p.value
 
 
-def slab_partition(nx: int, num_coarsenings: int, nranks: int, replicated_level: int = -1):
+def slab_partition(nx: int, ny: int, num_coarsenings: int, nranks: int, replicated_level: int = -1):
     """(first fine node column of every rank + [nx+1], replicated level)."""
     x0s = np.zeros(nranks + 1, np.int32)
     rep = C.c_int()
-    st = _lib.load().tmg_partition(nx, num_coarsenings, nranks, replicated_level, iptr(x0s), C.byref(rep))
+    st = _lib.load().tmg_partition(nx, ny, num_coarsenings, nranks, replicated_level, iptr(x0s), C.byref(rep))
     if st != 0:
         _raise(st, "tmg_partition failed")
     return x0s.tolist(), rep.value

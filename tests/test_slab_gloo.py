@@ -71,7 +71,7 @@ def _worker(rank, world, port, q):
     ug = rng.standard_normal(2 * (nx + 1) * (ny + 1))
     g = P.GridLevel(nx, ny)
     bc = P.wall_boundary_conditions(g, "uniform")
-    x0s, rep = P.slab_partition(nx, nc, world, replicated_level=1)
+    x0s, rep = P.slab_partition(nx, ny, nc, world, replicated_level=1)
     x0, x1 = x0s[rank], x0s[rank + 1]
     ncol = x1 - x0
     # owned node data, ghost columns filled by the exchange below
@@ -147,12 +147,24 @@ def test_slab_halo_apply_and_allreduce_over_gloo(world):
     assert len(x0s) == world + 1 and rep == 1
 
 
+def red_tx(nx, ny):
+    """Reduction tile width (tmg_gpu.cu red_tx_of): the fine strip width
+    rounded up to a power of two in [8, 64]."""
+    want = -(-(nx + 1) * -(-(ny + 1) // 128) // 1184)
+    tx = 8
+    while tx < 64 and tx < want:
+        tx *= 2
+    return tx
+
+
 def test_partition_invariants():
-    for nx, nc, n in [(8192, 10, 8), (2048, 8, 4), (512, 6, 2), (128, 4, 3)]:
-        x0s, rep = P.slab_partition(nx, nc, n)
-        gran = 1 << (nc - rep)
+    for nx, ny, nc, n in [(8192, 8192, 10, 8), (2048, 2048, 8, 4), (512, 512, 6, 2), (128, 64, 4, 3)]:
+        x0s, rep = P.slab_partition(nx, ny, nc, n)
+        gran = max(1 << (nc - rep), red_tx(nx, ny))
         assert x0s[0] == 0 and x0s[-1] == nx + 1
+        # slab boundaries never split a reduction tile or a coarse column pair
         assert all(x % gran == 0 for x in x0s[:-1])
         assert all(b - a >= 2 * gran for a, b in zip(x0s, x0s[1:]))
+    assert red_tx(8192, 8192) == 64 and red_tx(512, 512) == 8
     # one rank keeps every level global
-    assert P.slab_partition(64, 3, 1) == ([0, 65], 3)
+    assert P.slab_partition(64, 64, 3, 1) == ([0, 65], 3)
