@@ -657,30 +657,37 @@ __global__ void __launch_bounds__(kMarchThreads) k_march(MarchArgs a) {
   __syncthreads();
 
   double part = 0.0;
-  if (t >= kTY) {
-    // ---------------- producer warp: one lane issues every copy
-    if (t == kTY) {
-      int mis[Stage::NS];
-      uint32_t bytes[Stage::NS];
-      uint32_t total = 0;
+  // warp index through a shuffle: provably warp-uniform, so the producer
+  // branch is uniform and its values can stay in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, t >> 5, 0);
+  if (warp == kConsumerWarps) {
+    // ---------------- producer warp: every lane runs the loop, so the copy
+    // operands are warp-uniform and live in uniform registers; lane 0 issues
+    // (a single-lane loop made the compiler move each operand into a uniform
+    // register through a per-copy waterfall, ~25 instructions per copy)
+    const bool leader = (t == kTY);
+    int mis[Stage::NS];
+    uint32_t bytes[Stage::NS];
+    uint32_t total = 0;
 #pragma unroll
-      for (int k = 0; k < Stage::NS; ++k) {
-        const StreamDesc d = Stage::stream(a, k);
-        mis[k] = stream_mis(a, d, y0);
-        bytes[k] = static_cast<uint32_t>((d.n * d.esize + mis[k] + 15) / 16 * 16);
-        total += bytes[k];
+    for (int k = 0; k < Stage::NS; ++k) {
+      const StreamDesc d = Stage::stream(a, k);
+      mis[k] = stream_mis(a, d, y0);
+      bytes[k] = static_cast<uint32_t>((d.n * d.esize + mis[k] + 15) / 16 * 16);
+      total += bytes[k];
+    }
+    for (int j = 0; j < nent; ++j) {
+      const int s = j % kStages;
+      if (j >= kStages) mbar_wait(&empty[s], ((j / kStages) - 1) & 1);
+      const int c = cf + j;
+      // columns outside the padded storage (-1 .. nx+1) are not loaded
+      if (!in_storage(c)) {
+        if (leader) mbar_arrive(&full[s]);
+        continue;
       }
-      for (int j = 0; j < nent; ++j) {
-        const int s = j % kStages;
-        if (j >= kStages) mbar_wait(&empty[s], ((j / kStages) - 1) & 1);
-        const int c = cf + j;
-        // columns outside the padded storage (-1 .. nx+1) are not loaded
-        if (!in_storage(c)) {
-          mbar_arrive(&full[s]);
-          continue;
-        }
+      unsigned char* sl = slot(j);
+      if (leader) {
         mbar_expect_tx(&full[s], total);
-        unsigned char* sl = slot(j);
 #pragma unroll
         for (int k = 0; k < Stage::NS; ++k) {
           const StreamDesc d = Stage::stream(a, k);
@@ -688,6 +695,7 @@ __global__ void __launch_bounds__(kMarchThreads) k_march(MarchArgs a) {
           bulk_g2s(sl + Stage::off(k), src, bytes[k], &full[s]);
         }
       }
+      __syncwarp();
     }
   } else {
     // ---------------- consumers

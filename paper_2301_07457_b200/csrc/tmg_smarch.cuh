@@ -196,23 +196,27 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
                              static_cast<uintptr_t>(a.gc.idx(0, (y0 >> 1) + cr0)) * 16) & 15u);
   }
 
-  if (t >= kSY) {
-    if (t == kSY) {
-      const uint32_t bp = (kSRows * 8 + misS + 15) / 16 * 16;
-      const uint32_t bf = (kSRows * 16 + misF + 15) / 16 * 16;
-      const uint32_t bc = (kSCoarseRows * 16 + misC + 15) / 16 * 16;
-      const uint32_t total = kStencilPlanes * bp + bf + (UP ? bc : 0u);
-      for (int j = 0; j < nent; ++j) {
-        const int s = j % kSStages;
-        if (j >= kSStages) mbar_wait(&empty[s], ((j / kSStages) - 1) & 1);
-        const int c = cf + j;
-        if (!in_storage(c)) {
-          mbar_arrive(&full[s]);
-          continue;
-        }
+  // producer warp (identified through a shuffle, so the branch and the copy
+  // operands are warp-uniform and stay in uniform registers); lane 0 issues
+  if (__shfl_sync(0xffffffffu, t >> 5, 0) == kSWarps) {
+    const bool leader = (t == kSY);
+    const uint32_t bp = (kSRows * 8 + misS + 15) / 16 * 16;
+    const uint32_t bf = (kSRows * 16 + misF + 15) / 16 * 16;
+    const uint32_t bc = (kSCoarseRows * 16 + misC + 15) / 16 * 16;
+    const uint32_t total = kStencilPlanes * bp + bf + (UP ? bc : 0u);
+    for (int j = 0; j < nent; ++j) {
+      const int s = j % kSStages;
+      if (j >= kSStages) mbar_wait(&empty[s], ((j / kSStages) - 1) & 1);
+      const int c = cf + j;
+      if (!in_storage(c)) {
+        if (leader) mbar_arrive(&full[s]);
+        continue;
+      }
+      unsigned char* sl = slot(j);
+      const long ri = g.idx(c, y0 + r0);
+      if (leader) {
         mbar_expect_tx(&full[s], total);
-        unsigned char* sl = slot(j);
-        const long ri = g.idx(c, y0 + r0);
+#pragma unroll
         for (int k = 0; k < kStencilPlanes; ++k)
           bulk_g2s(sl + k * kSPlane, reinterpret_cast<const unsigned char*>(a.S + k * g.size + ri) - misS, bp,
                    &full[s]);
@@ -222,6 +226,7 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
           bulk_g2s(sl + kSO_C, reinterpret_cast<const unsigned char*>(a.uc + ci) - misC, bc, &full[s]);
         }
       }
+      __syncwarp();
     }
     return;
   }
