@@ -15,6 +15,7 @@
 //           iteration; one PCG iteration is a captured CUDA graph, the host
 //           only reads a 40-byte mirror of the PCG scalars to run the
 //           reference's stopping test (solvers.cpp:388) and error checks.
+#include <cudaTypedefs.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -815,6 +816,36 @@ void coarse_solve(H* h, Rank& R, const double2* f, double2* u) {
   h->count();
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time libcuda dependency)
+PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) fail(TMG_ERR_CUDA, "cuTensorMapEncodeTiled not available");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(p);
+  }();
+  return fn;
+}
+
+// the stencil planes of a level as a (padded row, storage column, plane)
+// tensor; one box = kSRows rows of one column, all planes (tmg_smarch.cuh)
+CUtensorMap stencil_tensor_map(const double* S, const Grid& g) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.P), static_cast<cuuint64_t>(g.size / g.P),
+                              static_cast<cuuint64_t>(kStencilPlanes)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.P) * 8, static_cast<cuuint64_t>(g.size) * 8};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(kSBoxRows), 1, static_cast<cuuint32_t>(kStencilPlanes)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(S), dims,
+                                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(TMG_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return m;
+}
+
 // two-stage marching kernels of a coarse (stencil) level: DOWN writes x2 into
 // `out` and f_c into the coarse rhs; UP prolongs u_c onto x2 and smooths twice
 template <bool UP>
@@ -824,6 +855,7 @@ void launch_smarch(H* h, Rank& R, int l, const double2* x2, const double2* uc, d
   long off;
   a.gc = coarse_of(h, R, l, off);
   a.S = R.lev[l].S;
+  a.tmS = stencil_tensor_map(a.S, a.g);
   a.f = R.lev[l].f;
   a.x2 = x2;
   a.uc = uc ? uc + off : nullptr;

@@ -28,6 +28,7 @@
 
 #include <cstdint>
 #include <type_traits>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "tmg_device.cuh"
@@ -46,6 +47,9 @@ constexpr int kSRows = kSY + 2;         // streamed rows per column
 constexpr long kSMinNodes = 200000;     // smaller levels: one-pass kernels
 
 struct SMarchArgs {
+  // the stencil planes as a 3-D tensor (padded row, storage column, plane):
+  // one TMA box of kSRows rows x 1 column x 19 planes per ring entry
+  CUtensorMap tmS;
   Grid g;   // the level
   Grid gc;  // its coarse level (restriction target / prolongation source)
   int tx;   // output columns per CTA (coarse columns for DOWN)
@@ -58,15 +62,22 @@ struct SMarchArgs {
   double omega;
 };
 
-// Slot layout: planes [19][kSRows], then f, then (UP) the coarse column. The
-// UP kernel's x2 is read by the threads directly (one column ahead) so that
-// six stages still fit two CTAs per SM.
-constexpr int kSPlane = sbytes(kSRows, 8);
+// Slot layout: planes [19][kSRows] (the TMA box, dense), then f, then (UP)
+// the coarse column; slots are 128-byte aligned for the tensor copy. The UP
+// kernel's x2 is read by the threads directly (one column ahead) so that six
+// stages still fit two CTAs per SM.
+// A box must start on a 16-byte boundary (an odd FP64 start row traps as an
+// illegal instruction), so it starts at the even row at or below the first
+// stream row and spans two extra rows; misS skips the leading one.
+constexpr int kSBoxRows = kSRows + 2;
+constexpr int kSPlane = kSBoxRows * 8;
+static_assert(kSPlane % 16 == 0, "TMA box rows must be a multiple of 16 bytes");
 constexpr int kSO_F = kStencilPlanes * kSPlane;
 constexpr int kSO_C = kSO_F + sbytes(kSRows, 16);
 constexpr int kSCoarseRows = kSRows / 2 + 3;
-constexpr int kSSlotDown = kSO_C;
-constexpr int kSSlotUp = kSO_C + sbytes(kSCoarseRows, 16);
+constexpr int round128(int b) { return (b + 127) / 128 * 128; }
+constexpr int kSSlotDown = round128(kSO_C);
+constexpr int kSSlotUp = round128(kSO_C + sbytes(kSCoarseRows, 16));
 
 // 2x2-block stencil application at row j of the centre column (cs = its
 // slot, ls = the left column's slot, both smem), window w (cols x-1..x+1,
@@ -135,8 +146,22 @@ __device__ __forceinline__ double2 s_jacobi_r(double2 x, double2 f, double2 y, d
   return make_double2(fma(omega * r.x, f.x - y.x, x.x), fma(omega * r.y, f.y - y.y, x.y));
 }
 
+// one box of the 3-D stencil tensor (all 19 planes of a column's row range)
+__device__ __forceinline__ void tma_planes(void* dst, const CUtensorMap* map, int row, int col, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(row), "r"(col), "r"(0), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// first stream row relative to y0 (R0 - 1, R0 = -1 UP / -2 DOWN)
 template <bool UP>
-__global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
+__host__ __device__ constexpr int r0c() { return (UP ? -1 : -2) - 1; }
+static_assert(kOY % 2 == 0 && (kSY - 2) % 2 == 0 && (kSY - 4) % 2 == 0, "even row tiles");
+
+template <bool UP>
+__global__ void __launch_bounds__(kSThreads) k_smarch(const __grid_constant__ SMarchArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int kSStages = s_stages<UP>();
   __shared__ uint64_t full[kSStages], empty[kSStages];
@@ -171,7 +196,8 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
   auto slot = [&](int j) { return smem_raw + static_cast<size_t>(j % kSStages) * kSlot; };
   auto in_storage = [&](int c) { return c >= -kGX && c < g.ncol + kGX; };
   // stream rows start at y0 + R0 - 1 (planes, f, x2); coarse rows at y0/2 + R0/2 - 2
-  const int r0 = R0 - 1;
+  constexpr int r0 = r0c<UP>();
+  static_assert(r0 == R0 - 1, "stream row offset");
   const int cr0 = (UP ? -2 : 0);
 
   if (t == 0) {
@@ -187,8 +213,10 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
   }
   __syncthreads();
 
-  const uintptr_t pS = reinterpret_cast<uintptr_t>(a.S), pf = reinterpret_cast<uintptr_t>(a.f);
-  const int misS = static_cast<int>((pS + static_cast<uintptr_t>(g.idx(0, y0 + r0)) * 8) & 15u);
+  const uintptr_t pf = reinterpret_cast<uintptr_t>(a.f);
+  // first stream row y0 + r0 in padded storage is y0 + r0 + kOY; y0 is even
+  // (kOwned is even), so its parity is that of r0 + kOY
+  constexpr int misS = ((r0c<UP>() + kOY) & 1) ? 8 : 0;
   const int misF = static_cast<int>((pf + static_cast<uintptr_t>(g.idx(0, y0 + r0)) * 16) & 15u);
   int misC = 0;
   if (UP) {
@@ -200,10 +228,10 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
   // operands are warp-uniform and stay in uniform registers); lane 0 issues
   if (__shfl_sync(0xffffffffu, t >> 5, 0) == kSWarps) {
     const bool leader = (t == kSY);
-    const uint32_t bp = (kSRows * 8 + misS + 15) / 16 * 16;
     const uint32_t bf = (kSRows * 16 + misF + 15) / 16 * 16;
     const uint32_t bc = (kSCoarseRows * 16 + misC + 15) / 16 * 16;
-    const uint32_t total = kStencilPlanes * bp + bf + (UP ? bc : 0u);
+    const uint32_t total = kStencilPlanes * kSPlane + bf + (UP ? bc : 0u);
+    if (leader) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.tmS)) : "memory");
     for (int j = 0; j < nent; ++j) {
       const int s = j % kSStages;
       if (j >= kSStages) mbar_wait(&empty[s], ((j / kSStages) - 1) & 1);
@@ -216,10 +244,8 @@ __global__ void __launch_bounds__(kSThreads) k_smarch(SMarchArgs a) {
       const long ri = g.idx(c, y0 + r0);
       if (leader) {
         mbar_expect_tx(&full[s], total);
-#pragma unroll
-        for (int k = 0; k < kStencilPlanes; ++k)
-          bulk_g2s(sl + k * kSPlane, reinterpret_cast<const unsigned char*>(a.S + k * g.size + ri) - misS, bp,
-                   &full[s]);
+        // padded row index y + kOY, storage column c + kGX (Grid::idx)
+        tma_planes(sl, &a.tmS, y0 + r0 + kOY - misS / 8, c + kGX, &full[s]);
         bulk_g2s(sl + kSO_F, reinterpret_cast<const unsigned char*>(a.f + ri) - misF, bf, &full[s]);
         if (UP) {
           const long ci = a.gc.idx((c + 1) >> 1, (y0 >> 1) + cr0);
