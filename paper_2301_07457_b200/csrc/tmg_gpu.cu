@@ -341,6 +341,11 @@ struct tmg_gpu_handle {
   // (graph[2]) and graph[k] opens by finishing iteration it-1
   cudaGraphExec_t graph[3] = {nullptr, nullptr, nullptr};
   long graph_kernels[3] = {0, 0, 0};
+  // kernels before the conditional stopping test (all of them without one)
+  long graph_head_kernels[3] = {0, 0, 0};
+  // device-side stopping test between the fused update and the rest of an
+  // iteration (TMG_NO_COND_NODES=1 turns it off, for A/B timing)
+  bool cond_nodes = true;
   int g_gamma = -1, g_pre = -1, g_post = -1;
   bool g_fused = false;
   // node columns per tile of the fine-level reductions (red_tiles)
@@ -894,7 +899,7 @@ void launch_smarch(H* h, Rank& R, int l, const double2* x2, const double2* uc, d
 // neighbours; the finest replicated level is assembled from the ranks' owned
 // columns after the restriction.
 bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp zr_op = kRedNone,
-                   int upd_k = -1) {
+                   int upd_k = -1, const std::function<void()>& after_update = nullptr) {
   auto& rs = h->ranks;
   if (l == 0) {
     for (Rank* R : rs) coarse_solve(h, *R, R->lev[0].f, R->lev[0].u[R->lev[0].cur]);
@@ -929,6 +934,7 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
     flip();
     s = 2;
     zero = false;
+    if (after_update) after_update();
   } else if (fine && zero && pre >= 2) {
     // the finest f (the PCG residual) already carries its halo
     for (Rank* R : rs) {
@@ -1084,12 +1090,47 @@ void capture_iteration(H* h, int gamma, int pre, int post) {
       R->fine().f = fused_upd ? R->rbuf(k) : R->r;
     }
     cudaGraph_t g = nullptr;
-    CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    // iterations that open with the fused update get a device-side stopping
+    // test: the rest of the iteration is the body of a conditional node
+    const bool cond = fused_upd && !first && h->cond_nodes;
+    long head_kernels = -1;
+    std::function<void()> split;
+    if (cond) {
+      CK(cudaGraphCreate(&g, 0));
+      cudaGraphConditionalHandle hc;
+      CK(cudaGraphConditionalHandleCreate(&hc, g, 0, cudaGraphCondAssignDefault));
+      CK(cudaStreamBeginCaptureToGraph(h->stream, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      split = [h, hc, &head_kernels] {
+        // every rank holds the same r.r, so all take the same branch
+        k_set_continue<<<1, 1, 0, h->stream>>>(hc, h->ranks[0]->st);
+        CKL();
+        h->count();
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t cg = nullptr;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t ndeps = 0;
+        CK(cudaStreamGetCaptureInfo(h->stream, &cs, nullptr, &cg, &deps, &ndeps));
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = hc;
+        cp.conditional.type = cudaGraphCondTypeIf;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, cg, deps, ndeps, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        cudaGraph_t done = nullptr;
+        CK(cudaStreamEndCapture(h->stream, &done));
+        head_kernels = h->capture_kernels;
+        CK(cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      };
+    } else {
+      CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    }
     h->capturing = true;
     h->capture_kernels = 0;
     try {
       // z = M^-1 r: one cycle from z = 0 (solvers.cpp:523-527), fused with z.r
-      const bool fused = enqueue_cycle(h, nc, true, gamma, pre, post, kRedZr, (fused_upd && !first) ? k : -1);
+      const bool fused = enqueue_cycle(h, nc, true, gamma, pre, post, kRedZr, (fused_upd && !first) ? k : -1, split);
       auto z = [&](Rank& R) { return R.fine().u[R.fine().cur]; };
       if (!fused) dot(h, z, [&](Rank& R) { return R.fine().f; }, kRedZr, false);
       // p = z + beta p; Ap; pAp; alpha (solvers.cpp:367-382)
@@ -1122,16 +1163,25 @@ void capture_iteration(H* h, int gamma, int pre, int post) {
       }
     } catch (...) {
       h->capturing = false;
-      cudaStreamEndCapture(h->stream, &g);
+      cudaGraph_t part = nullptr;
+      cudaStreamEndCapture(h->stream, &part);
+      if (part && part != g) cudaGraphDestroy(part);
       if (g) cudaGraphDestroy(g);
       for (Rank* R : h->ranks) R->fine().f = R->r;
       throw;
     }
     h->capturing = false;
-    CK(cudaStreamEndCapture(h->stream, &g));
+    if (cond) {
+      cudaGraph_t body = nullptr;
+      CK(cudaStreamEndCapture(h->stream, &body));  // the body belongs to g
+      if (head_kernels < 0) fail(TMG_ERR_CUDA, "conditional iteration graph without its update pass");
+    } else {
+      CK(cudaStreamEndCapture(h->stream, &g));
+    }
     CK(cudaGraphInstantiate(&h->graph[g_slot], g, 0));
     cudaGraphDestroy(g);
     h->graph_kernels[g_slot] = h->capture_kernels;
+    h->graph_head_kernels[g_slot] = cond ? head_kernels : h->capture_kernels;
     for (Rank* R : h->ranks) R->fine().f = R->r;
   };
   capture(0);
@@ -1251,7 +1301,7 @@ void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int 
   auto bvec = [&](Rank& R) { return R.b; };
   dot(h, bvec, bvec, kRedB, false);
   for (Rank* R : h->ranks) {
-    k_pcg_begin<<<1, 1, 0, h->stream>>>(R->st);
+    k_pcg_begin<<<1, 1, 0, h->stream>>>(R->st, tol);
     CKL();
     h->count();
     const Level& F = R->fine();
@@ -1310,11 +1360,15 @@ void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int 
       for (int it = 1; it <= max_iter; ++it) {
         const int gs = (fu && it == 1) ? 2 : (it - 1) & 1;
         CK(cudaGraphLaunch(h->graph[gs], h->stream));
-        h->launches += h->graph_kernels[gs];
         CK(cudaStreamSynchronize(h->stream));
         // fused: this graph opened by finishing iteration it-1; its residual
-        // decides before anything iteration `it` computed speculatively
-        if (fu && it >= 2 && record(it - 1)) break;
+        // decides before anything iteration `it` computed speculatively (the
+        // graph's conditional node already skipped that work on the device)
+        if (fu && it >= 2 && record(it - 1)) {
+          h->launches += h->graph_head_kernels[gs];
+          break;
+        }
+        h->launches += h->graph_kernels[gs];
         const int status = m->status;
         if (status == 4) {
           char buf[200];
@@ -1448,6 +1502,7 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
                           static_cast<int>(StSweep01U::kSlot * kStages)));
   CK(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking));
   if (const char* v = std::getenv("TMG_SMARCH_MIN_NODES")) hp->smarch_min_nodes = std::atol(v);
+  if (const char* v = std::getenv("TMG_NO_COND_NODES")) hp->cond_nodes = std::atoi(v) == 0;
   for (cudaEvent_t& e : hp->ev) CK(cudaEventCreate(&e));
   for (int i = 0; i < nlocal; ++i) {
     hp->own.push_back(std::make_unique<Rank>());

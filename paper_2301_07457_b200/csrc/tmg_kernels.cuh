@@ -43,6 +43,7 @@ __device__ __forceinline__ double block_sum(double v) {
 // Scalars of the PCG recurrence (pcg_solve, solvers.cpp:332-395), resident on
 // the device so iterations chain without host round trips.
 struct PcgState {
+  double tol;  // stopping tolerance of the running solve (device-side stopping test)
   double bnorm;
   double rr, zr, zr_prev, pap, alpha, beta, relres;
   int it;      // iteration being computed (1-based)
@@ -602,11 +603,22 @@ __global__ void k_sub(const double2* __restrict__ b, const double2* __restrict__
   }
 }
 
-__global__ void k_pcg_begin(PcgState* st) {
+__global__ void k_pcg_begin(PcgState* st, double tol) {
+  st->tol = tol;
   st->it = 1;
   st->status = 0;
   st->zr_prev = 0.0;
   st->beta = 0.0;
+}
+
+// Device-side stopping test between the fused update pass and the rest of a
+// PCG iteration graph: r_{it-1} is complete once StSweep01U has run, and when
+// it meets the test (solvers.cpp:388) the rest of the iteration (the V-cycle
+// and the p-update, speculative work the host would discard) is skipped by
+// the graph's conditional node.
+__global__ void k_set_continue(cudaGraphConditionalHandle hc, const PcgState* st) {
+  const double rel = st->relres;
+  cudaGraphSetConditional(hc, (rel <= st->tol || rel == 0.0) ? 0u : 1u);
 }
 
 // ------------------------------------------------------ consumers (K9-K11)

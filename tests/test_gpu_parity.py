@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import paper_2301_07457_b200 as P
-from helpers import MAT, pair, rel
+from helpers import MAT, moduli, pair, rel
 from oracle import pyoracle as po
 
 pytestmark = pytest.mark.gpu
@@ -314,3 +314,27 @@ def test_device_simp_matches_host_moduli():
     x = np.random.default_rng(9).standard_normal(g.dof_count())
     ya, yb = a.apply(3, x), b_.apply(3, x)
     assert np.max(np.abs(ya - yb)) <= 1e-14 * np.max(np.abs(yb))
+
+
+@pytest.mark.parametrize("tol,max_iter", [(1e-8, 500), (1e-12, 6), (1e-3, 500)])
+def test_device_stopping_test_matches_host_loop(monkeypatch, tol, max_iter):
+    """The iteration graphs skip the speculative rest of an iteration on the
+    device once r_{it-1} meets the stopping test (a conditional graph node).
+    The results must be bitwise those of the plain graphs (TMG_NO_COND_NODES),
+    at convergence, at the iteration cap and on an early stop."""
+    nx = ny = 128
+    _, E = moduli(nx, ny, "iid", 4)
+    g = P.GridLevel(nx, ny)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    b = P.assemble_rhs(g, bc)
+    cfg = P.SolverConfig(tol=tol, max_iter=max_iter)
+    reps = []
+    for off in ("0", "1"):
+        monkeypatch.setenv("TMG_NO_COND_NODES", off)
+        ops = P.MultigridOperators(g, 4, 0.3, bc)
+        ops.set_moduli(E, 0.6)
+        reps.append((P.pcgmg_solve(ops, b, cfg), P.compliance(ops)))
+    (a, ca), (c, cc) = reps
+    assert a.iterations == c.iterations and a.converged == c.converged
+    assert a.residual_history == c.residual_history
+    assert np.array_equal(a.solution, c.solution) and ca == cc
