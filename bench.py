@@ -46,6 +46,9 @@ CONFIGS = {
            "c2: 2048x2048 Q4 wall, 16x16-element phase checkerboard seed 2 (1e9 contrast), 9 levels, tol 1e-8"),
     "c1": (512, 512, 6, "iid", 0,
            "c1: 512x512 Q4 wall, iid U(0,1) densities seed 0, 7 levels, tol 1e-8"),
+    # the optimizer config c3's mesh and hierarchy, one solve (latency-bound sizes)
+    "c3": (1024, 1024, 7, "iid", 0,
+           "c3 mesh: 1024x1024 Q4 wall, iid U(0,1) densities seed 0, 8 levels, tol 1e-8"),
 }
 TOL, OMEGA, SWEEPS, MAX_ITER = 1e-8, 0.6, 2, 5000
 MATERIAL = dict(phase_moduli=[1.0, 0.5, 0.2, 1e-9], poisson_ratio=0.3, penalty=3.0)

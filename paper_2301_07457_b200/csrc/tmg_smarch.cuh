@@ -44,7 +44,10 @@ constexpr int kSThreads = kSY + 32;     // + one producer warp
 template <bool UP>
 __host__ __device__ constexpr int s_stages() { return 6; }
 constexpr int kSRows = kSY + 2;         // streamed rows per column
-constexpr long kSMinNodes = 200000;     // smaller levels: one-pass kernels
+// every coarse level runs the two-stage kernels (measured on c1-c4: one-pass
+// kernels for the small levels were 1-13 % slower per PCG iteration); the
+// one-pass kernels remain for W-cycle revisits and other sweep counts
+constexpr long kSMinNodes = 0;
 
 struct SMarchArgs {
   // the stencil planes as a 3-D tensor (padded row, storage column, plane):
