@@ -61,10 +61,11 @@ def test_c2_solution_residual_under_reference_K(c2):
     6e-6 under its own K (measured at 256^2 - 1024^2 with this recipe), and
     the iteration count at which the recursive residual crosses 1e-8 is
     chaotic (reported, not gated). Gated: the device solution's true residual
-    under the checker's assembled K is at that attainable level, and its
-    residuals under the two operators differ by no more than the rounding of
-    the products: |r_ref - r_dev| <= 64 eps || |K| |u| || / ||b|| (the device
-    Ke is <= 1 ulp from the quadrature Ke, and both sum 18 terms per row)."""
+    under the checker's assembled K is at that attainable level, and its true
+    residuals under the two operators agree to 5 %. (The naive rounding bound
+    64 eps |||K||u|||/||b|| is ~3e-4 here, useless against 4e-6 residuals:
+    K u cancels over nine orders of magnitude. Measured differences of the
+    two residuals are 0.8-1.2 %, i.e. 3-6e-8 absolute.)"""
     ops, sysc, b, nc = c2
     rep = P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-8, max_iter=2000, num_coarsenings=nc))
     assert rep.converged
@@ -72,11 +73,7 @@ def test_c2_solution_residual_under_reference_K(c2):
     r_ref = np.linalg.norm(b - sysc.matvec(nc, rep.solution)) / nb
     r_dev = np.linalg.norm(b - ops.apply(nc, rep.solution)) / nb
     assert r_ref <= 1e-5
-    off, col, val = sysc.csr(nc)
-    rows = np.repeat(np.arange(off.size - 1), np.diff(off))
-    absku = np.bincount(rows, weights=np.abs(val) * np.abs(rep.solution[col]), minlength=off.size - 1)
-    bound = 64 * np.finfo(float).eps * np.linalg.norm(absku) / nb
-    assert abs(r_ref - r_dev) <= bound, (r_ref, r_dev, bound)
+    assert abs(r_ref - r_dev) <= 0.05 * r_ref, (r_ref, r_dev)
 
 
 @pytest.fixture(scope="module")
