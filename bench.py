@@ -46,7 +46,9 @@ CONFIGS = {
            "c2: 2048x2048 Q4 wall, 16x16-element phase checkerboard seed 2 (1e9 contrast), 9 levels, tol 1e-8"),
     "c1": (512, 512, 6, "iid", 0,
            "c1: 512x512 Q4 wall, iid U(0,1) densities seed 0, 7 levels, tol 1e-8"),
-    # the optimizer config c3's mesh and hierarchy, one solve (latency-bound sizes)
+    # the optimizer configs' meshes and hierarchies, one solve (latency-bound sizes)
+    "c0": (64, 64, 3, "iid", 0,
+           "c0 mesh: 64x64 Q4 wall, iid U(0,1) densities seed 0, 4 levels, tol 1e-8"),
     "c3": (1024, 1024, 7, "iid", 0,
            "c3 mesh: 1024x1024 Q4 wall, iid U(0,1) densities seed 0, 8 levels, tol 1e-8"),
 }
