@@ -1222,10 +1222,15 @@ void setup(H* h, double omega) {
       dim3 blk(32, 4), grd((cg.ny + 1 + 31) / 32, (cg.ncol + 3) / 4);
       // the output pointer is offset by `off` nodes inside every plane; the
       // plane stride stays that of the stored level
-      with_op(*R, l, [&](auto op) {
-        k_galerkin<decltype(op)><<<grd, blk, 0, h->stream>>>(op, R->lev[l].g, cg, R->lev[l - 1].S + off,
-                                                             R->lev[l - 1].g.size);
-      });
+      if (l == h->nc) {
+        k_galerkin_cells<<<grd, blk, 0, h->stream>>>(R->fine_op(), R->lev[l].g, cg, R->lev[l - 1].S + off,
+                                                     R->lev[l - 1].g.size);
+      } else {
+        with_op(*R, l, [&](auto op) {
+          k_galerkin<decltype(op)><<<grd, blk, 0, h->stream>>>(op, R->lev[l].g, cg, R->lev[l - 1].S + off,
+                                                               R->lev[l - 1].g.size);
+        });
+      }
       CKL();
       h->count();
     }
@@ -1630,6 +1635,30 @@ int tmg_gpu_set_problem(tmg_gpu_handle* h, double nu, const int* fixed_dofs, int
     tmg_element_stiffness(1.0, nu, h->ke);
     CK(cudaMemcpyToSymbolAsync(c_k8, h->ke, 8 * sizeof(double), 0, cudaMemcpyHostToDevice, h->stream));  // row 0
     CK(cudaMemcpyToSymbolAsync(c_ke64, h->ke, 64 * sizeof(double), 0, cudaMemcpyHostToDevice, h->stream));
+    // M_q = (1/4) P_q^T Ke P_q of the four element quadrants of a coarse cell
+    // (k_galerkin_cells), from the Ke the device applies (8 values, ke_perm)
+    {
+      double mq[4][64];
+      auto w1 = [](int f, int cc) { return f == 2 * cc ? 1.0L : (f == 1 ? 0.5L : 0.0L); };
+      const int cx[4] = {0, 1, 1, 0}, cy[4] = {0, 0, 1, 1};  // corner -> (x, y)
+      for (int q = 0; q < 4; ++q) {
+        const int qx = q & 1, qy = q >> 1;
+        long double Pm[8][8] = {};  // fine dof (2k+d) <- coarse dof (2m+d)
+        for (int k = 0; k < 4; ++k)
+          for (int m = 0; m < 4; ++m) {
+            const long double w = w1(qx + cx[k], cx[m]) * w1(qy + cy[k], cy[m]);
+            for (int d = 0; d < 2; ++d) Pm[2 * k + d][2 * m + d] = w;
+          }
+        for (int a = 0; a < 8; ++a)
+          for (int b = 0; b < 8; ++b) {
+            long double acc = 0.0L;
+            for (int r = 0; r < 8; ++r)
+              for (int c = 0; c < 8; ++c) acc += Pm[r][a] * static_cast<long double>(h->ke[ke_perm(r, c)]) * Pm[c][b];
+            mq[q][a * 8 + b] = static_cast<double>(0.25L * acc);
+          }
+      }
+      CK(cudaMemcpyToSymbolAsync(c_mq, mq, sizeof(mq), 0, cudaMemcpyHostToDevice, h->stream));
+    }
     CK(cudaStreamSynchronize(h->stream));
     h->have_problem = true;
     h->have_setup = false;

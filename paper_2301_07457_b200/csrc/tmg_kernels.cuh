@@ -330,12 +330,7 @@ __host__ __device__ constexpr double pw(int o) { return o == 0 ? 1.0 : 0.5; }
 // of j are always inside I's 3x3 coarse neighbourhood. Only the centre and the
 // four forward blocks are stored (symmetry).
 template <class Op>
-__global__ void __launch_bounds__(128) k_galerkin(Op fine, Grid fg, Grid cg, double* __restrict__ Sc,
-                                                  long LSc) {
-  const int Y = blockIdx.x * 32 + threadIdx.x;
-  const int X = blockIdx.y * 4 + threadIdx.y;
-  if (X >= cg.ncol || Y > cg.ny) return;
-  double acc[5][4];
+__device__ __forceinline__ void galerkin_gather(const Op& fine, const Grid& fg, int X, int Y, double (&acc)[5][4]) {
 #pragma unroll
   for (int a = 0; a < 5; ++a)
 #pragma unroll
@@ -391,6 +386,85 @@ __global__ void __launch_bounds__(128) k_galerkin(Op fine, Grid fg, Grid cg, dou
         }
       }
     }
+  }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(128) k_galerkin(Op fine, Grid fg, Grid cg, double* __restrict__ Sc,
+                                                  long LSc) {
+  const int Y = blockIdx.x * 32 + threadIdx.x;
+  const int X = blockIdx.y * 4 + threadIdx.y;
+  if (X >= cg.ncol || Y > cg.ny) return;
+  double acc[5][4];
+  galerkin_gather(fine, fg, X, Y, acc);
+  const long I = cg.idx(X, Y);
+  Sc[0 * LSc + I] = acc[0][0];
+  Sc[1 * LSc + I] = acc[0][1];
+  Sc[2 * LSc + I] = acc[0][3];
+#pragma unroll
+  for (int s = 1; s < 5; ++s)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Sc[(3 + 4 * (s - 1) + q) * LSc + I] = acc[s][q];
+}
+
+// Level nc-1 from the fine level, per coarse cell. Every fine element lies in
+// one coarse cell C and its nodes interpolate from C's four corners only, so
+// away from fixed dofs (1/4) P^T A P = sum_C sum_q E_{C,q} M_q with four
+// constant 8x8 matrices M_q = (1/4) P_q^T Ke P_q (q = the element's quadrant
+// of C; c_mq, built on the host from the device Ke). A coarse node's five
+// stored blocks then cost 144 FMAs over the 4x4 moduli around it instead of
+// the 81-block gather of k_galerkin. Nodes with a fixed dof among the 5x5
+// fine nodes around them take the general gather (identity rows, masks).
+__constant__ double c_mq[4][64];
+
+__global__ void __launch_bounds__(128) k_galerkin_cells(FineOp fine, Grid fg, Grid cg, double* __restrict__ Sc,
+                                                        long LSc) {
+  const int Y = blockIdx.x * 32 + threadIdx.x;
+  const int X = blockIdx.y * 4 + threadIdx.y;
+  if (X >= cg.ncol || Y > cg.ny) return;
+  const long c = fg.idx(2 * X, 2 * Y);
+  bool fixed = false;
+#pragma unroll
+  for (int dx = -2; dx <= 2; ++dx)
+#pragma unroll
+    for (int dy = -2; dy <= 2; ++dy) fixed = fixed || fine.M[c + dx * fg.P + dy] != 0;
+  double acc[5][4];
+  if (fixed) {
+    galerkin_gather(fine, fg, X, Y, acc);
+  } else {
+    // moduli of the 4x4 fine elements around the node: e[u][v] = element
+    // (2X - 2 + u, 2Y - 2 + v)
+    double e[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) e[u][v] = fine.E[c + (u - 2) * fg.P + (v - 2)];
+    // block (a, b) of cell (cx, cy) (offsets 0/1 from X-1, Y-1), summed into acc[slot]
+    auto cell = [&](int cx, int cy, int a, int b, double (&out)[4]) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double w = e[2 * cx + (q & 1)][2 * cy + (q >> 1)];
+        out[0] = fma(w, c_mq[q][(2 * a) * 8 + 2 * b], out[0]);
+        out[1] = fma(w, c_mq[q][(2 * a) * 8 + 2 * b + 1], out[1]);
+        out[2] = fma(w, c_mq[q][(2 * a + 1) * 8 + 2 * b], out[2]);
+        out[3] = fma(w, c_mq[q][(2 * a + 1) * 8 + 2 * b + 1], out[3]);
+      }
+    };
+#pragma unroll
+    for (int k = 0; k < 5; ++k)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) acc[k][m] = 0.0;
+    // corners: (0,0)->0 (1,0)->1 (1,1)->2 (0,1)->3; cell (1,1) is (X, Y)
+    cell(0, 0, 2, 2, acc[0]);  // centre: I is corner 2 of (X-1, Y-1)
+    cell(1, 0, 3, 3, acc[0]);  //         corner 3 of (X, Y-1)
+    cell(1, 1, 0, 0, acc[0]);  //         corner 0 of (X, Y)
+    cell(0, 1, 1, 1, acc[0]);  //         corner 1 of (X-1, Y)
+    cell(0, 1, 1, 2, acc[1]);  // N
+    cell(1, 1, 0, 3, acc[1]);
+    cell(1, 0, 3, 1, acc[2]);  // SE
+    cell(1, 0, 3, 2, acc[3]);  // E
+    cell(1, 1, 0, 1, acc[3]);
+    cell(1, 1, 0, 2, acc[4]);  // NE
   }
   const long I = cg.idx(X, Y);
   Sc[0 * LSc + I] = acc[0][0];
