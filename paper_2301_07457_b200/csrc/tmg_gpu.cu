@@ -1304,7 +1304,8 @@ void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int 
   capture_iteration(h, gamma, pre, post);
   CK(cudaEventRecord(h->ev[0], h->stream));
   auto bvec = [&](Rank& R) { return R.b; };
-  dot(h, bvec, bvec, kRedB, false);
+  // without x0, r = b bitwise, so b.b is also r.r (the plain value lands in scal)
+  dot(h, bvec, bvec, kRedB, !use_x0);
   for (Rank* R : h->ranks) {
     k_pcg_begin<<<1, 1, 0, h->stream>>>(R->st, tol);
     CKL();
@@ -1329,7 +1330,7 @@ void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int 
   }
   halo_vec(h, nc, [&](Rank& R) { return R.r; });
   auto rvec = [&](Rank& R) { return R.r; };
-  dot(h, rvec, rvec, kRedPlain, true);
+  if (use_x0) dot(h, rvec, rvec, kRedPlain, true);
   Rank& R0 = *h->ranks[0];
   PcgState st0;
   CK(cudaMemcpyAsync(&st0, R0.st, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
