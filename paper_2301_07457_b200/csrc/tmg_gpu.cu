@@ -1092,7 +1092,9 @@ void capture_iteration(H* h, int gamma, int pre, int post) {
     cudaGraph_t g = nullptr;
     // iterations that open with the fused update get a device-side stopping
     // test: the rest of the iteration is the body of a conditional node
-    const bool cond = fused_upd && !first && h->cond_nodes;
+    // (NCCL collectives stay out of conditional bodies: that transport cannot
+    // be exercised on a one-GPU box, so its graphs keep the plain form)
+    const bool cond = fused_upd && !first && h->cond_nodes && (!h->comm || h->comm->local());
     long head_kernels = -1;
     std::function<void()> split;
     if (cond) {
