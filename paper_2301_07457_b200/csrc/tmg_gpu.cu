@@ -1209,6 +1209,18 @@ void finish_update(H* h, int it) {
   });
 }
 
+// dense Cholesky of the coarsest matrix, in shared memory when it fits
+void launch_cholesky(cudaStream_t s, double* A, int n, int* bad_row) {
+  if (n <= kCholSmemMax) {
+    const size_t sm = sizeof(double) * n * n;
+    CK(cudaFuncSetAttribute(k_cholesky<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    k_cholesky<true><<<1, 1024, sm, s>>>(A, n, bad_row);
+  } else {
+    k_cholesky<false><<<1, 1024, 0, s>>>(A, n, bad_row);
+  }
+  CKL();
+}
+
 // ----------------------------------------------------------------- setup --
 
 void setup(H* h, double omega) {
@@ -1257,7 +1269,7 @@ void setup(H* h, double omega) {
       k_dense_assemble<decltype(op)><<<dim3((g0.ny + 1 + 63) / 64, g0.nx + 1), 64, 0, h->stream>>>(op, g0, R->A0, n);
     });
     CKL();
-    k_cholesky<<<1, 1024, 0, h->stream>>>(R->A0, n, R->bad_row);
+    launch_cholesky(h->stream, R->A0, n, R->bad_row);
     CKL();
     h->count(2);
   }

@@ -503,10 +503,18 @@ __global__ void k_dense_assemble(Op op, Grid g, double* __restrict__ A, int n) {
 // Right-looking Cholesky, lower triangle in place, one CTA (n <= 2048).
 // A non-positive pivot records its row like CholeskyFactor::factor
 // (solvers.cpp:144-148).
-__global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ A, int n, int* bad_row) {
+// SMEM: the matrix is factored in shared memory (n <= kCholSmemMax; the
+// same operations in the same order, so the factor is bit-identical).
+constexpr int kCholSmemMax = 168;  // 168^2 doubles = 220.5 KB
+template <bool SMEM>
+__global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ Ag, int n, int* bad_row) {
+  extern __shared__ double As[];
   __shared__ int fail;
   const int t = threadIdx.x, nt = blockDim.x;
   const int lane = t & 31, w = t >> 5, nw = nt >> 5;
+  double* A = SMEM ? As : Ag;
+  if (SMEM)
+    for (int k = t; k < n * n; k += nt) As[k] = Ag[k];
   if (t == 0) fail = -1;
   __syncthreads();
   for (int k = 0; k < n; ++k) {
@@ -526,6 +534,10 @@ __global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ A, int n
       for (int j = k + 1 + lane; j <= i; j += 32) Ai[j] -= lik * A[static_cast<long>(j) * n + k];
     }
     __syncthreads();
+  }
+  if (SMEM) {
+    __syncthreads();
+    for (int k = t; k < n * n; k += nt) Ag[k] = As[k];
   }
   if (t == 0) *bad_row = fail;
 }

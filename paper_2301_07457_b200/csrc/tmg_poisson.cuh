@@ -444,7 +444,7 @@ void p_setup(PH* h, double omega) {
   CK(cudaMemsetAsync(h->A0, 0, sizeof(double) * n * n, h->stream));
   k_p_dense<<<p_grid(C.g), kPT, 0, h->stream>>>(C.S, C.g, h->A0, n);
   CKL();
-  k_cholesky<<<1, 1024, 0, h->stream>>>(h->A0, n, h->bad_row);
+  launch_cholesky(h->stream, h->A0, n, h->bad_row);
   CKL();
   int bad = -1;
   CK(cudaMemcpyAsync(&bad, h->bad_row, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
