@@ -383,13 +383,27 @@ using H = tmg_gpu_handle;
 // strip width for the whole fine level (strip_tx below, the same formula),
 // rounded up to a power of two. It depends on the global mesh only, so every
 // partition tiles the fine level identically.
-int red_tx_of(int nx, int ny) {
-  const long rows_tiles = (ny + 1L + kRedRows - 1) / kRedRows;
-  const long want = ((nx + 1L) * rows_tiles + 148 * 8 - 1) / (148 * 8);
-  int tx = 8;
-  while (tx < 64 && tx < want) tx *= 2;
-  return tx;
+// Strip width of the fine marching passes: the power of two in [1, 64]
+// minimising waves x (a*tx + 3) column steps for a nominal 3 resident CTAs on
+// each of 148 SMs (ties to the wider strip). On c1-c4 it is the width the
+// passes used before (8-64); meshes of ~64^2 get 1-column strips, whose
+// passes are 4 column steps long instead of 11.
+int pow2_strip(long rows_tiles, long cols, int a) {
+  const long slots = 3L * 148;
+  int best = 64;
+  long best_cost = -1;
+  for (int tx = 64; tx >= 1; tx /= 2) {
+    const long ctas = rows_tiles * ((cols + tx - 1) / tx);
+    const long cost = ((ctas + slots - 1) / slots) * (a * tx + 3);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = tx;
+    }
+  }
+  return best;
 }
+
+int red_tx_of(int nx, int ny) { return pow2_strip((ny + 1L + kRedRows - 1) / kRedRows, nx + 1L, 1); }
 
 // Fine node-column partition: boundaries multiples of 2^(nc - rep), so every
 // distributed level has even slab boundaries, and of the reduction tile
@@ -636,10 +650,7 @@ void reduce(H* h, RedOp op, const std::function<void(Rank&, RedOp, double*)>& la
 // Output columns per fine-level marching CTA: short strips (many waves of
 // 3-5 resident CTAs per SM) balance best; measured on c4, one-wave long
 // strips ran 10-25% slower for these kernels.
-int strip_tx(long rows_tiles, long cols) {
-  const long want = (cols * rows_tiles + 148 * 8 - 1) / (148 * 8);
-  return static_cast<int>(std::min<long>(64, std::max<long>(6, want)));
-}
+int strip_tx(long rows_tiles, long cols, int a = 1) { return pow2_strip(rows_tiles, cols, a); }
 
 // Resident CTAs of one marching kernel on the whole device (occupancy x SMs;
 // cached per kernel: every handle of a process runs on the same GPU type).
@@ -710,7 +721,7 @@ void launch_march(H* h, MarchArgs a) {
   const size_t sm = static_cast<size_t>(Stage::kSlot) * kStages;
   if constexpr (Stage::kRow0 == -1) {  // restriction: tiles of coarse rows / columns
     const long ty = (a.gc.ny + 1 + Stage::kOwned / 2 - 1) / (Stage::kOwned / 2);
-    a.tx = strip_tx(ty, a.gc.ncol);
+    a.tx = strip_tx(ty, a.gc.ncol, 2);
     grid = dim3(ty, (a.gc.ncol + a.tx - 1) / a.tx);
   } else {
     const long ty = (a.g.ny + 1 + Stage::kOwned - 1) / Stage::kOwned;

@@ -148,13 +148,15 @@ def test_slab_halo_apply_and_allreduce_over_gloo(world):
 
 
 def red_tx(nx, ny):
-    """Reduction tile width (tmg_gpu.cu red_tx_of): the fine strip width
-    rounded up to a power of two in [8, 64]."""
-    want = -(-(nx + 1) * -(-(ny + 1) // 128) // 1184)
-    tx = 8
-    while tx < 64 and tx < want:
-        tx *= 2
-    return tx
+    """Reduction tile width (tmg_gpu.cu red_tx_of / pow2_strip): the power of
+    two in [1, 64] minimising waves x (tx + 3) for 3 x 148 resident CTAs."""
+    rows_tiles, cols, slots = -(-(ny + 1) // 128), nx + 1, 3 * 148
+    best, best_cost = 64, None
+    for tx in (64, 32, 16, 8, 4, 2, 1):
+        cost = -(-rows_tiles * -(-cols // tx) // slots) * (tx + 3)
+        if best_cost is None or cost < best_cost:
+            best, best_cost = tx, cost
+    return best
 
 
 def test_partition_invariants():
@@ -165,6 +167,6 @@ def test_partition_invariants():
         # slab boundaries never split a reduction tile or a coarse column pair
         assert all(x % gran == 0 for x in x0s[:-1])
         assert all(b - a >= 2 * gran for a, b in zip(x0s, x0s[1:]))
-    assert red_tx(8192, 8192) == 64 and red_tx(512, 512) == 8
+    assert red_tx(8192, 8192) == 64 and red_tx(512, 512) == 8 and red_tx(64, 64) == 1
     # one rank keeps every level global
     assert P.slab_partition(64, 64, 3, 1) == ([0, 65], 3)
