@@ -7,6 +7,10 @@ hierarchy here, so the device is compared against it directly: Galerkin
 levels, one V(2,2)-cycle, and the GPU solution's residual under the
 checker's assembled K.
 
+c3 (1024^2, r_f 3, warm start, 8 levels): the optimizer closed loop for its
+first five outer iterations against the checker (bit-exact to the
+reference's optimize(); ~25 s of CPU per outer iteration).
+
 c4 (8192^2, 134M DOFs, 11 levels, the bench workload): size-independent
 properties only: the residual recomputed through a different kernel (the
 plain K.u pass) against the host right-hand side, compliance = b.u at
@@ -114,3 +118,22 @@ def test_c4_preconditioner_symmetric(c4):
     my = P.mg_cycle(ops, zero, y, 1, 2, 2)
     lhs, rhs = float(y @ mx), float(x @ my)
     assert abs(lhs - rhs) <= 1e-10 * max(abs(lhs), abs(rhs))
+
+
+def test_c3_first_outer_iterations():
+    n, nc, k = 1024, 7, 5
+    g = P.GridLevel(n, n)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    phases = [1.0, 0.5, 0.2, 1e-9]
+    fr = [0.15, 0.15, 0.15, 0.55]
+    mat = P.MaterialModel(phase_moduli=phases, poisson_ratio=0.3, penalty=3.0)
+    cfg = P.OptimConfig(volume_fractions=fr, filter_radius=3.0, warm_start=True, tol=1e-12, max_outer=k,
+                        solver=P.SolverConfig(tol=1e-8, max_iter=2000, num_coarsenings=nc))
+    ops = P.MultigridOperators(g, nc, 0.3, bc)
+    got = P.optimize(ops, mat, cfg)
+    want = po.optimize("orc", n, n, list(bc.fixed_dofs), list(bc.point_loads), phases, 3.0, 0.3, fr,
+                       num_coarsenings=nc, filter_radius=3.0, tol=1e-12, warm_start=True, max_outer=k)
+    assert got.outer_iterations == want["outer_iterations"] == k
+    np.testing.assert_allclose(got.compliance_history, want["compliance_history"], rtol=1e-9)
+    assert all(abs(a - b) <= 2 for a, b in zip(got.solver_iteration_history, want["solver_iteration_history"]))
+    assert np.max(np.abs(got.density - want["density"])) <= 1e-8

@@ -112,6 +112,8 @@ CASES = [
     (64, 64, 3, "checker", 2, "uniform"),
     (128, 64, 4, "iid", 3, "uniform"),
     (256, 256, 5, "iid", 0, "uniform"),
+    (512, 512, 6, "iid", 0, "uniform"),  # BASELINE c1 exactly (7 levels, seed 0)
+    (1024, 1024, 7, "uniform", 0, "uniform"),  # BASELINE c3's first solve (initial design)
 ]
 
 
