@@ -164,6 +164,12 @@ struct Rank {
   PcgState* st = nullptr;
   HostMirror* hm = nullptr;      // pinned, mapped
   HostMirror* hm_dev = nullptr;  // device alias of hm
+  // device-side PCG loop: its record and residual history (pinned, mapped)
+  LoopRecord* lrec = nullptr;
+  LoopRecord* lrec_dev = nullptr;
+  double* hist = nullptr;
+  double* hist_dev = nullptr;
+  int hist_cap = 0;
   double* scal = nullptr;        // device scalars: [0] result, [1] rank partial, [2] global sum
   double* scal_host = nullptr;   // pinned
   // scratch for consumers
@@ -346,6 +352,12 @@ struct tmg_gpu_handle {
   // device-side stopping test between the fused update and the rest of an
   // iteration (TMG_NO_COND_NODES=1 turns it off, for A/B timing)
   bool cond_nodes = true;
+  // the whole PCG loop as one graph with a conditional WHILE node (fused
+  // scheme, conditional nodes on); the host launches it once per solve
+  // (TMG_NO_DEVICE_LOOP=1 keeps the per-iteration host loop)
+  bool device_loop = true;
+  cudaGraphExec_t loop = nullptr;
+  long loop_first_kernels = 0, loop_head_kernels = 0, loop_rest_kernels = 0;
   int g_gamma = -1, g_pre = -1, g_post = -1;
   bool g_fused = false;
   // node columns per tile of the fine-level reductions (red_tiles)
@@ -511,6 +523,8 @@ void free_rank(Rank& R) {
                   static_cast<void*>(R.aux), static_cast<void*>(R.aux2), static_cast<void*>(R.ocbuf)})
     cudaFree(p);
   if (R.hm) cudaFreeHost(R.hm);
+  if (R.lrec) cudaFreeHost(R.lrec);
+  if (R.hist) cudaFreeHost(R.hist);
   if (R.scal_host) cudaFreeHost(R.scal_host);
 }
 
@@ -519,6 +533,7 @@ void free_handle(H* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (cudaGraphExec_t gx : h->graph)
     if (gx) cudaGraphExecDestroy(gx);
+  if (h->loop) cudaGraphExecDestroy(h->loop);
   h->comm.reset();
   for (Rank* R : h->ranks) free_rank(*R);
   for (cudaEvent_t e : h->ev)
@@ -605,6 +620,9 @@ void alloc_rank(H* h, Rank& R) {
   std::memset(R.hm, 0, sizeof(HostMirror));
   CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.hm_dev), R.hm, 0));
   CK(cudaHostAlloc(&R.scal_host, 4 * sizeof(double), cudaHostAllocDefault));
+  CK(cudaHostAlloc(&R.lrec, sizeof(LoopRecord), cudaHostAllocMapped));
+  std::memset(R.lrec, 0, sizeof(LoopRecord));
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.lrec_dev), R.lrec, 0));
 }
 
 // ------------------------------------------------------------- exchanges ---
@@ -1076,6 +1094,156 @@ void dot(H* h, const std::function<const double2*(Rank&)>& a, const std::functio
       want_out);
 }
 
+// Buffer roles of a captured PCG iteration of direction-buffer parity k:
+// every level's iterate starts in u[0]; iteration it smooths against
+// r_{it-1}, which lives in rbuf((it-1)&1) under the fused update.
+void set_iteration_roles(H* h, int k, bool fused_upd) {
+  for (Rank* R : h->ranks) {
+    for (Level& L : R->lev) L.cur = 0;
+    R->fine().f = fused_upd ? R->rbuf(k) : R->r;
+  }
+}
+
+// The kernels of one PCG iteration (pcg_solve loop body, solvers.cpp:359-391)
+// on parity k, enqueued on the (capturing) stream. `split` runs right after
+// the fused update pass that opens an iteration it >= 2.
+void enqueue_iteration(H* h, int k, bool first, bool fused_upd, int gamma, int pre, int post,
+                       const std::function<void()>& split) {
+  const int nc = h->nc;
+  // z = M^-1 r: one cycle from z = 0 (solvers.cpp:523-527), fused with z.r
+  const bool fused = enqueue_cycle(h, nc, true, gamma, pre, post, kRedZr, (fused_upd && !first) ? k : -1, split);
+  auto z = [&](Rank& R) { return R.fine().u[R.fine().cur]; };
+  if (!fused) dot(h, z, [&](Rank& R) { return R.fine().f; }, kRedZr, false);
+  // p = z + beta p; Ap; pAp; alpha (solvers.cpp:367-382)
+  halo_vec(h, nc, z);
+  reduce(h, kRedPap, [&](Rank& R, RedOp rop, double* out) {
+    MarchArgs a = march_args(h, R, z(R));
+    a.u2 = R.pbuf[k];
+    a.out0 = R.pbuf[k ^ 1];
+    a.out1 = R.ap;
+    a.rop = rop;
+    a.red_out = out;
+    launch_march<StPupd, true>(h, a);
+  });
+  halo_vec(h, nc, [&](Rank& R) { return R.pbuf[k ^ 1]; });
+  if (fused_upd) {
+    // x and r are updated by the next iteration's first pass (or by
+    // finish_update after the last one); it reads A p with halo
+    halo_vec(h, nc, [&](Rank& R) { return R.ap; });
+  } else {
+    // x += alpha p; r -= alpha Ap; rr (solvers.cpp:383-386)
+    reduce(h, kRedRr, [&](Rank& R, RedOp rop, double* out) {
+      const Grid& g = R.fine().g;
+      k_update_xr<<<red_launch_grid(h, g), kRedRows, 0, h->stream>>>(R.x, R.r, R.pbuf[k ^ 1], R.ap, g,
+                                                                     red_tiles(h, g), R.partials, R.rticket, rop,
+                                                                     R.st, R.hm_dev, out);
+      CKL();
+      h->count();
+    });
+    halo_vec(h, nc, [&](Rank& R) { return R.r; });
+  }
+}
+
+// The graph being captured on the handle's stream.
+cudaGraph_t capturing_graph(H* h) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t cg = nullptr;
+  CK(cudaStreamGetCaptureInfo(h->stream, &cs, nullptr, &cg, nullptr, nullptr));
+  return cg;
+}
+
+// Appends a conditional node on `hc` after everything captured so far, ends
+// that capture and continues capturing into the node's body.
+void capture_into_conditional(H* h, cudaGraphConditionalHandle hc, cudaGraphConditionalNodeType type) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t cg = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  CK(cudaStreamGetCaptureInfo(h->stream, &cs, nullptr, &cg, &deps, &ndeps));
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = hc;
+  cp.conditional.type = type;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CK(cudaGraphAddNode(&node, cg, deps, ndeps, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaGraph_t done = nullptr;
+  CK(cudaStreamEndCapture(h->stream, &done));
+  CK(cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+}
+
+// The whole PCG loop of the fused scheme as one graph:
+//   iteration 1; tail
+//   WHILE (loop) {
+//     update(it-1) [StSweep01U]; head: IF (rest) { rest of iteration it (parity 1); tail:
+//       IF (next) { update(it); head: IF (rest) { rest of iteration it+1 (parity 0); tail } } }
+//   }
+// k_loop_head records the residual history and applies the stopping test and
+// the iteration cap; k_loop_tail stops on a breakdown (kernels in
+// tmg_kernels.cuh). The kernels are those of the per-iteration graphs, so
+// the results are bitwise the same; the host launches once and reads the
+// LoopRecord.
+void capture_loop(H* h, int gamma, int pre, int post) {
+  Rank& R0 = *h->ranks[0];
+  cudaGraph_t G = nullptr;
+  CK(cudaGraphCreate(&G, 0));
+  cudaGraphConditionalHandle hw;
+  CK(cudaGraphConditionalHandleCreate(&hw, G, 0, cudaGraphCondAssignDefault));
+  h->capturing = true;
+  h->capture_kernels = 0;
+  long head_k = 0, rest_k = 0, first_k = 0;
+  try {
+    CK(cudaStreamBeginCaptureToGraph(h->stream, G, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    set_iteration_roles(h, 0, true);
+    enqueue_iteration(h, 0, true, true, gamma, pre, post, nullptr);
+    k_loop_tail<<<1, 1, 0, h->stream>>>(hw, hw, R0.st, R0.lrec_dev);
+    CKL();
+    h->count();
+    first_k = h->capture_kernels;
+    capture_into_conditional(h, hw, cudaGraphCondTypeWhile);
+    auto iteration = [&](int k, bool last) {
+      set_iteration_roles(h, k, true);
+      const long k0 = h->capture_kernels;
+      auto split = [&] {
+        cudaGraphConditionalHandle hr;
+        CK(cudaGraphConditionalHandleCreate(&hr, capturing_graph(h), 0, cudaGraphCondAssignDefault));
+        k_loop_head<<<1, 1, 0, h->stream>>>(hr, hw, R0.st, R0.lrec_dev);
+        CKL();
+        h->count();
+        head_k = h->capture_kernels - k0;
+        capture_into_conditional(h, hr, cudaGraphCondTypeIf);
+      };
+      enqueue_iteration(h, k, false, true, gamma, pre, post, split);
+      cudaGraphConditionalHandle next = hw;
+      if (!last) CK(cudaGraphConditionalHandleCreate(&next, capturing_graph(h), 0, cudaGraphCondAssignDefault));
+      k_loop_tail<<<1, 1, 0, h->stream>>>(next, hw, R0.st, R0.lrec_dev);
+      CKL();
+      h->count();
+      rest_k = h->capture_kernels - k0 - head_k;
+      if (!last) capture_into_conditional(h, next, cudaGraphCondTypeIf);
+    };
+    iteration(1, false);  // it = 2, 4, ...: r_{it-1} in rbuf(1)
+    iteration(0, true);   // it = 3, 5, ...
+    cudaGraph_t body = nullptr;
+    CK(cudaStreamEndCapture(h->stream, &body));
+  } catch (...) {
+    h->capturing = false;
+    cudaGraph_t part = nullptr;
+    cudaStreamEndCapture(h->stream, &part);
+    cudaGraphDestroy(G);
+    for (Rank* R : h->ranks) R->fine().f = R->r;
+    throw;
+  }
+  h->capturing = false;
+  for (Rank* R : h->ranks) R->fine().f = R->r;
+  CK(cudaGraphInstantiate(&h->loop, G, 0));
+  cudaGraphDestroy(G);
+  h->loop_first_kernels = first_k;
+  h->loop_head_kernels = head_k;
+  h->loop_rest_kernels = rest_k;
+}
+
 // One PCG iteration (pcg_solve loop body, solvers.cpp:359-391) as a graph.
 // Two graphs alternate the roles of the two direction buffers, because the
 // fused p-update reads the old p around each node while writing the new one.
@@ -1085,27 +1253,27 @@ void capture_iteration(H* h, int gamma, int pre, int post) {
     if (gx) cudaGraphExecDestroy(gx);
     gx = nullptr;
   }
+  if (h->loop) cudaGraphExecDestroy(h->loop);
+  h->loop = nullptr;
   const int nc = h->nc;
   // fused update: the first fine pass is the two-sweep stage, which then
   // also finishes the previous iteration (StSweep01U)
   // (a one-level hierarchy has no smoothing pass: its cycle is the direct solve)
   const bool fused_upd = pre >= 2 && nc >= 1;
+  // conditional nodes: not with NCCL collectives inside their bodies (that
+  // transport cannot be exercised on a one-GPU box, so its graphs keep the
+  // plain form)
+  const bool cond_ok = fused_upd && h->cond_nodes && (!h->comm || h->comm->local());
   // graph slot g: 0/1 = iterations with (it-1)&1 == g (it >= 2 when fused),
   // 2 = iteration 1 of the fused scheme
   auto capture = [&](int g_slot) {
     const int k = g_slot & 1;
     const bool first = g_slot == 2;
-    for (Rank* R : h->ranks) {
-      for (Level& L : R->lev) L.cur = 0;
-      // iteration it smooths against r_{it-1}, which lives in rbuf((it-1)&1)
-      R->fine().f = fused_upd ? R->rbuf(k) : R->r;
-    }
+    set_iteration_roles(h, k, fused_upd);
     cudaGraph_t g = nullptr;
     // iterations that open with the fused update get a device-side stopping
     // test: the rest of the iteration is the body of a conditional node
-    // (NCCL collectives stay out of conditional bodies: that transport cannot
-    // be exercised on a one-GPU box, so its graphs keep the plain form)
-    const bool cond = fused_upd && !first && h->cond_nodes && (!h->comm || h->comm->local());
+    const bool cond = cond_ok && !first;
     long head_kernels = -1;
     std::function<void()> split;
     if (cond) {
@@ -1118,23 +1286,8 @@ void capture_iteration(H* h, int gamma, int pre, int post) {
         k_set_continue<<<1, 1, 0, h->stream>>>(hc, h->ranks[0]->st);
         CKL();
         h->count();
-        cudaStreamCaptureStatus cs;
-        cudaGraph_t cg = nullptr;
-        const cudaGraphNode_t* deps = nullptr;
-        size_t ndeps = 0;
-        CK(cudaStreamGetCaptureInfo(h->stream, &cs, nullptr, &cg, &deps, &ndeps));
-        cudaGraphNodeParams cp{};
-        cp.type = cudaGraphNodeTypeConditional;
-        cp.conditional.handle = hc;
-        cp.conditional.type = cudaGraphCondTypeIf;
-        cp.conditional.size = 1;
-        cudaGraphNode_t node;
-        CK(cudaGraphAddNode(&node, cg, deps, ndeps, &cp));
-        cudaGraph_t body = cp.conditional.phGraph_out[0];
-        cudaGraph_t done = nullptr;
-        CK(cudaStreamEndCapture(h->stream, &done));
         head_kernels = h->capture_kernels;
-        CK(cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        capture_into_conditional(h, hc, cudaGraphCondTypeIf);
       };
     } else {
       CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
@@ -1142,38 +1295,7 @@ void capture_iteration(H* h, int gamma, int pre, int post) {
     h->capturing = true;
     h->capture_kernels = 0;
     try {
-      // z = M^-1 r: one cycle from z = 0 (solvers.cpp:523-527), fused with z.r
-      const bool fused = enqueue_cycle(h, nc, true, gamma, pre, post, kRedZr, (fused_upd && !first) ? k : -1, split);
-      auto z = [&](Rank& R) { return R.fine().u[R.fine().cur]; };
-      if (!fused) dot(h, z, [&](Rank& R) { return R.fine().f; }, kRedZr, false);
-      // p = z + beta p; Ap; pAp; alpha (solvers.cpp:367-382)
-      halo_vec(h, nc, z);
-      reduce(h, kRedPap, [&](Rank& R, RedOp rop, double* out) {
-        MarchArgs a = march_args(h, R, z(R));
-        a.u2 = R.pbuf[k];
-        a.out0 = R.pbuf[k ^ 1];
-        a.out1 = R.ap;
-        a.rop = rop;
-        a.red_out = out;
-        launch_march<StPupd, true>(h, a);
-      });
-      halo_vec(h, nc, [&](Rank& R) { return R.pbuf[k ^ 1]; });
-      if (fused_upd) {
-        // x and r are updated by the next iteration's first pass (or by
-        // finish_update after the last one); it reads A p with halo
-        halo_vec(h, nc, [&](Rank& R) { return R.ap; });
-      } else {
-        // x += alpha p; r -= alpha Ap; rr (solvers.cpp:383-386)
-        reduce(h, kRedRr, [&](Rank& R, RedOp rop, double* out) {
-          const Grid& g = R.fine().g;
-          k_update_xr<<<red_launch_grid(h, g), kRedRows, 0, h->stream>>>(R.x, R.r, R.pbuf[k ^ 1], R.ap, g,
-                                                                         red_tiles(h, g), R.partials, R.rticket,
-                                                                         rop, R.st, R.hm_dev, out);
-          CKL();
-          h->count();
-        });
-        halo_vec(h, nc, [&](Rank& R) { return R.r; });
-      }
+      enqueue_iteration(h, k, first, fused_upd, gamma, pre, post, split);
     } catch (...) {
       h->capturing = false;
       cudaGraph_t part = nullptr;
@@ -1200,6 +1322,7 @@ void capture_iteration(H* h, int gamma, int pre, int post) {
   capture(0);
   capture(1);
   if (fused_upd) capture(2);
+  if (cond_ok && h->device_loop) capture_loop(h, gamma, pre, post);
   h->g_gamma = gamma;
   h->g_pre = pre;
   h->g_post = post;
@@ -1327,12 +1450,25 @@ void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int 
   if (pre < 0) fail(TMG_ERR_CONFIG, "smoothing sweep counts must be non-negative");
   const int nc = h->nc;
   capture_iteration(h, gamma, pre, post);
+  const bool dloop = h->loop && max_iter >= 1;
+  if (dloop) {
+    // the device loop writes residual_history[1 .. iterations] here
+    Rank& R0 = *h->ranks[0];
+    if (R0.hist_cap < max_iter + 1) {
+      if (R0.hist) CK(cudaFreeHost(R0.hist));
+      R0.hist = nullptr;
+      R0.hist_cap = 0;
+      CK(cudaHostAlloc(&R0.hist, sizeof(double) * (max_iter + 1), cudaHostAllocMapped));
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R0.hist_dev), R0.hist, 0));
+      R0.hist_cap = max_iter + 1;
+    }
+  }
   CK(cudaEventRecord(h->ev[0], h->stream));
   auto bvec = [&](Rank& R) { return R.b; };
   // without x0, r = b bitwise, so b.b is also r.r (the plain value lands in scal)
   dot(h, bvec, bvec, kRedB, !use_x0);
   for (Rank* R : h->ranks) {
-    k_pcg_begin<<<1, 1, 0, h->stream>>>(R->st, tol);
+    k_pcg_begin<<<1, 1, 0, h->stream>>>(R->st, tol, max_iter, R->hist_dev);
     CKL();
     h->count();
     const Level& F = R->fine();
@@ -1374,6 +1510,31 @@ void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int 
     o.hist.push_back(rel);
     if (rel <= tol) {
       o.converged = 1;
+    } else if (dloop) {
+      // the whole loop on the device: one launch, one synchronisation
+      LoopRecord* lr = R0.lrec;
+      std::memset(lr, 0, sizeof(LoopRecord));
+      CK(cudaGraphLaunch(h->loop, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      LoopRecord rec;
+      std::memcpy(&rec, lr, sizeof rec);  // written by the device before the synchronisation
+      h->launches += h->loop_first_kernels + rec.heads * h->loop_head_kernels +
+                     std::max(0, rec.rests - 1) * h->loop_rest_kernels;
+      if (rec.status == 4) {
+        char buf[200];
+        std::snprintf(buf, sizeof buf, "preconditioner is not positive definite: z^T r = %f at iteration %d",
+                      rec.zr, rec.err_it);
+        fail(TMG_ERR_PRECONDITIONER, buf);
+      }
+      if (rec.status == 3) {
+        char buf[200];
+        std::snprintf(buf, sizeof buf, "PCG breakdown: p^T A p = %f at iteration %d", rec.pap, rec.err_it);
+        fail(TMG_ERR_DEFINITENESS, buf);
+      }
+      o.hist.insert(o.hist.end(), R0.hist + 1, R0.hist + 1 + rec.iterations);
+      o.iterations = rec.iterations;
+      o.converged = rec.converged;
+      o.final_residual = o.hist.back();
     } else {
       const bool fu = h->g_fused;
       const volatile HostMirror* m = R0.hm;
@@ -1534,6 +1695,7 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
   CK(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking));
   if (const char* v = std::getenv("TMG_SMARCH_MIN_NODES")) hp->smarch_min_nodes = std::atol(v);
   if (const char* v = std::getenv("TMG_NO_COND_NODES")) hp->cond_nodes = std::atoi(v) == 0;
+  if (const char* v = std::getenv("TMG_NO_DEVICE_LOOP")) hp->device_loop = std::atoi(v) == 0;
   for (cudaEvent_t& e : hp->ev) CK(cudaEventCreate(&e));
   for (int i = 0; i < nlocal; ++i) {
     hp->own.push_back(std::make_unique<Rank>());

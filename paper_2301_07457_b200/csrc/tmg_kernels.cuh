@@ -44,6 +44,8 @@ __device__ __forceinline__ double block_sum(double v) {
 // the device so iterations chain without host round trips.
 struct PcgState {
   double tol;  // stopping tolerance of the running solve (device-side stopping test)
+  double* hist;  // device-side loop: residual history (mapped pinned host memory)
+  int max_iter;  // device-side loop: iteration cap
   double bnorm;
   double rr, zr, zr_prev, pap, alpha, beta, relres;
   int it;      // iteration being computed (1-based)
@@ -689,8 +691,10 @@ __global__ void k_sub(const double2* __restrict__ b, const double2* __restrict__
   }
 }
 
-__global__ void k_pcg_begin(PcgState* st, double tol) {
+__global__ void k_pcg_begin(PcgState* st, double tol, int max_iter, double* hist) {
   st->tol = tol;
+  st->max_iter = max_iter;
+  st->hist = hist;
   st->it = 1;
   st->status = 0;
   st->zr_prev = 0.0;
@@ -705,6 +709,54 @@ __global__ void k_pcg_begin(PcgState* st, double tol) {
 __global__ void k_set_continue(cudaGraphConditionalHandle hc, const PcgState* st) {
   const double rel = st->relres;
   cudaGraphSetConditional(hc, (rel <= st->tol || rel == 0.0) ? 0u : 1u);
+}
+
+// ---- the whole PCG loop as one graph (a conditional WHILE node whose body
+// runs two iterations, one per direction-buffer parity). The host launches it
+// once per solve and reads this record when it completes.
+struct LoopRecord {
+  int iterations;  // completed iterations
+  int converged;
+  int status;      // 0, or the first breakdown (PcgState::status codes)
+  int err_it;      // iteration of the breakdown
+  double zr, pap;  // their values (error messages)
+  int heads, rests;  // executed heads (update + test) and rests (instrumentation)
+};
+
+// After the fused update that completes iteration st->it - 1: record its
+// relative residual (residual_history, solvers.cpp:388-391) and run the rest
+// of iteration st->it unless the stopping test holds or max_iter iterations
+// are complete (pcg_solve's loop bound, solvers.cpp:359); stopping also ends
+// the WHILE loop.
+__global__ void k_loop_head(cudaGraphConditionalHandle rest, cudaGraphConditionalHandle loop, const PcgState* st,
+                            LoopRecord* rec) {
+  const int done = st->it - 1;
+  const double rel = st->relres;
+  st->hist[done] = rel;
+  rec->iterations = done;
+  rec->heads += 1;
+  const bool conv = rel <= st->tol || rel == 0.0;
+  rec->converged = conv ? 1 : 0;
+  const bool go = !conv && done < st->max_iter;
+  cudaGraphSetConditional(rest, go ? 1u : 0u);
+  if (!go) cudaGraphSetConditional(loop, 0u);
+}
+
+// After the rest of iteration st->it: a breakdown (z.r <= 0 or p.Ap <= 0,
+// solvers.cpp:362-380) ends the loop; otherwise `next` (the following
+// iteration's guard, or the WHILE handle) lets it continue.
+__global__ void k_loop_tail(cudaGraphConditionalHandle next, cudaGraphConditionalHandle loop, const PcgState* st,
+                            LoopRecord* rec) {
+  rec->rests += 1;
+  const bool ok = st->status == 0;
+  if (!ok) {
+    rec->status = st->status;
+    rec->err_it = st->it;
+    rec->zr = st->zr;
+    rec->pap = st->pap;
+    cudaGraphSetConditional(loop, 0u);
+  }
+  cudaGraphSetConditional(next, ok ? 1u : 0u);
 }
 
 // ------------------------------------------------------ consumers (K9-K11)

@@ -595,7 +595,7 @@ int tmg_poisson_solve(tmg_poisson_handle* h, const double* b, const double* x0, 
     CK(cudaEventRecord(h->ev[0], h->stream));
     p_upload(h->stream, h->b, b, F.g);
     CK(cudaMemsetAsync(h->p[0], 0, sizeof(double) * n, h->stream));
-    k_pcg_begin<<<1, 1, 0, h->stream>>>(h->st, tol);
+    k_pcg_begin<<<1, 1, 0, h->stream>>>(h->st, tol, max_iter, nullptr);
     CKL();
     k_p_dot<<<kRedBlocks, kRedThreads, 0, h->stream>>>(h->b, h->b, n, h->partials, h->ticket, kRedB, h->st,
                                                       h->hm_dev, nullptr);

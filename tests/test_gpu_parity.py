@@ -318,12 +318,15 @@ def test_device_simp_matches_host_moduli():
     assert np.max(np.abs(ya - yb)) <= 1e-14 * np.max(np.abs(yb))
 
 
-@pytest.mark.parametrize("tol,max_iter", [(1e-8, 500), (1e-12, 6), (1e-3, 500)])
-def test_device_stopping_test_matches_host_loop(monkeypatch, tol, max_iter):
+@pytest.mark.parametrize("tol,max_iter", [(1e-8, 500), (1e-12, 6), (1e-12, 1), (1e-12, 2), (1e-3, 500)])
+@pytest.mark.parametrize("switch", ["TMG_NO_COND_NODES", "TMG_NO_DEVICE_LOOP"])
+def test_device_stopping_test_matches_host_loop(monkeypatch, switch, tol, max_iter):
     """The iteration graphs skip the speculative rest of an iteration on the
     device once r_{it-1} meets the stopping test (a conditional graph node).
     The results must be bitwise those of the plain graphs (TMG_NO_COND_NODES),
-    at convergence, at the iteration cap and on an early stop."""
+    at convergence, at the iteration cap and on an early stop. The same holds
+    for the whole loop as one graph (a conditional WHILE node, the default)
+    against the per-iteration host loop (TMG_NO_DEVICE_LOOP)."""
     nx = ny = 128
     _, E = moduli(nx, ny, "iid", 4)
     g = P.GridLevel(nx, ny)
@@ -332,7 +335,7 @@ def test_device_stopping_test_matches_host_loop(monkeypatch, tol, max_iter):
     cfg = P.SolverConfig(tol=tol, max_iter=max_iter)
     reps = []
     for off in ("0", "1"):
-        monkeypatch.setenv("TMG_NO_COND_NODES", off)
+        monkeypatch.setenv(switch, off)
         ops = P.MultigridOperators(g, 4, 0.3, bc)
         ops.set_moduli(E, 0.6)
         reps.append((P.pcgmg_solve(ops, b, cfg), P.compliance(ops)))
@@ -340,3 +343,24 @@ def test_device_stopping_test_matches_host_loop(monkeypatch, tol, max_iter):
     assert a.iterations == c.iterations and a.converged == c.converged
     assert a.residual_history == c.residual_history
     assert np.array_equal(a.solution, c.solution) and ca == cc
+
+
+@pytest.mark.parametrize("omega", [1.2, 2.0])
+@pytest.mark.parametrize("device_loop", ["0", "1"])
+def test_breakdown_raises_like_reference(monkeypatch, omega, device_loop):
+    """An over-relaxed smoother makes the V-cycle indefinite: the reference
+    throws PreconditionerError with z^T r and the iteration (solvers.cpp:
+    362-366), at iteration 2 for omega 1.2 and at iteration 1 for 2.0 on this
+    mesh. The device loop (one graph) and the host loop raise the same."""
+    import re
+
+    monkeypatch.setenv("TMG_NO_DEVICE_LOOP", "0" if device_loop == "1" else "1")
+    ops, sysc, b, _, _ = pair(32, 32, 2, seed=4, omega=omega)
+    with pytest.raises(po.OracleError) as want:
+        sysc.solve(b, tol=1e-8, max_iter=300)
+    with pytest.raises(P.PreconditionerError) as got:
+        P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-8, max_iter=300))
+    pat = r"z\^T r = (-?[0-9.]+) at iteration (\d+)"
+    (zw, iw), (zg, ig) = re.search(pat, str(want.value)).groups(), re.search(pat, str(got.value)).groups()
+    assert iw == ig
+    assert abs(float(zg) - float(zw)) <= 1e-6 * abs(float(zw))
