@@ -36,6 +36,7 @@
 #include "tmg_kernels.cuh"
 #include "tmg_march.cuh"
 #include "tmg_smarch.cuh"
+#include "tmg_stile.cuh"
 #include "tmg_oc.cuh"
 
 using namespace tmg;
@@ -365,6 +366,9 @@ struct tmg_gpu_handle {
   // coarse levels at least this large use the two-stage kernels
   // (TMG_SMARCH_MIN_NODES overrides it, for tests on small meshes)
   long smarch_min_nodes = kSMinNodes;
+  // coarse levels up to this many nodes run the V(2,2) halves as shared-memory
+  // tiles instead of marching kernels (tmg_stile.cuh)
+  long stile_max_nodes = kTileMaxNodes;
   // instrumentation
   long launches = 0;
   bool capturing = false;
@@ -912,7 +916,14 @@ void launch_smarch(H* h, Rank& R, int l, const double2* x2, const double2* uc, d
     a.tx = march_tx(ty, a.g.ncol, slots, 1, 7, true);
     grid = dim3(ty, (a.g.ncol + a.tx - 1) / a.tx);
   }
-  k_smarch<UP><<<grid, kSThreads, sm, h->stream>>>(a);
+  if (!h->dist(l) && static_cast<long>(a.g.nx + 1) * (a.g.ny + 1) <= h->stile_max_nodes) {
+    // small level: one shared-memory tile per CTA (tmg_stile.cuh)
+    grid = UP ? dim3((a.g.ny + kTU) / kTU, (a.g.ncol + kTU - 1) / kTU)
+              : dim3((a.gc.ny + kTC) / kTC, (a.gc.ncol + kTC - 1) / kTC);
+    k_stile<UP><<<grid, kTThreads, t_smem<UP>(), h->stream>>>(a);
+  } else {
+    k_smarch<UP><<<grid, kSThreads, sm, h->stream>>>(a);
+  }
   CKL();
   h->count();
 }
@@ -1690,10 +1701,13 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
                           static_cast<int>(kSSlotDown * s_stages<false>())));
   CK(cudaFuncSetAttribute(k_smarch<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(kSSlotUp * s_stages<true>())));
+  CK(cudaFuncSetAttribute(k_stile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<false>()));
+  CK(cudaFuncSetAttribute(k_stile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<true>()));
   CK(cudaFuncSetAttribute(k_march<StSweep01U, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(StSweep01U::kSlot * kStages)));
   CK(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking));
   if (const char* v = std::getenv("TMG_SMARCH_MIN_NODES")) hp->smarch_min_nodes = std::atol(v);
+  if (const char* v = std::getenv("TMG_STILE_MAX_NODES")) hp->stile_max_nodes = std::atol(v);
   if (const char* v = std::getenv("TMG_NO_COND_NODES")) hp->cond_nodes = std::atoi(v) == 0;
   if (const char* v = std::getenv("TMG_NO_DEVICE_LOOP")) hp->device_loop = std::atoi(v) == 0;
   for (cudaEvent_t& e : hp->ev) CK(cudaEventCreate(&e));

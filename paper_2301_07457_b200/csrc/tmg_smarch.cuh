@@ -93,7 +93,8 @@ struct SPlanes {
   }
 };
 
-__device__ __forceinline__ void s_fwd(const SPlanes& p, int k, int j, double2 v, double& y0, double& y1) {
+template <class PL>
+__device__ __forceinline__ void s_fwd(const PL& p, int k, int j, double2 v, double& y0, double& y1) {
   y0 = fma(p.at(k, j), v.x, y0);
   y0 = fma(p.at(k + 1, j), v.y, y0);
   y1 = fma(p.at(k + 2, j), v.x, y1);
@@ -118,8 +119,8 @@ struct LCache {
 // Three independent accumulator pairs (centre/N/SE, E/NE/S, NW/W/SW) keep
 // three FMA chains in flight per thread; with two resident CTAs a single
 // chain per dof left the FP64 pipe waiting on its own latency.
-template <class LP>
-__device__ __forceinline__ void s_apply(const SPlanes& C, const LP& L, int j, const double2 (&l)[3],
+template <class CP, class LP>
+__device__ __forceinline__ void s_apply(const CP& C, const LP& L, int j, const double2 (&l)[3],
                                         const double2 (&c)[3], const double2 (&r)[3], double2& y, double2& d) {
   const double c00 = C.at(0, j), c01 = C.at(1, j), c11 = C.at(2, j);
   double a0 = c00 * c[1].x, a1 = c01 * c[1].x;

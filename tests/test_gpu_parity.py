@@ -364,3 +364,29 @@ def test_breakdown_raises_like_reference(monkeypatch, omega, device_loop):
     (zw, iw), (zg, ig) = re.search(pat, str(want.value)).groups(), re.search(pat, str(got.value)).groups()
     assert iw == ig
     assert abs(float(zg) - float(zw)) <= 1e-6 * abs(float(zw))
+
+
+@pytest.mark.parametrize("nx,ny,nc,recipe,gamma", [(64, 64, 3, "iid", 1), (256, 128, 5, "checker", 1),
+                                                   (96, 160, 4, "iid", 2), (1024, 512, 7, "iid", 1)])
+def test_tile_kernels_match_marching(monkeypatch, nx, ny, nc, recipe, gamma):
+    """Small coarse levels run the V(2,2) halves as shared-memory tiles
+    (tmg_stile.cuh) with the marching kernels' per-node arithmetic, so every
+    result is bitwise that of the marching path (TMG_STILE_MAX_NODES=0)."""
+    _, E = moduli(nx, ny, recipe, 3)
+    g = P.GridLevel(nx, ny)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    b = P.assemble_rhs(g, bc)
+    cfg = P.SolverConfig(tol=1e-10, max_iter=500, gamma=gamma)
+    f = np.random.default_rng(2).standard_normal(b.size)
+    reps = []
+    for lim in ("1000000000", "0"):
+        monkeypatch.setenv("TMG_STILE_MAX_NODES", lim)
+        ops = P.MultigridOperators(g, nc, 0.3, bc)
+        ops.set_moduli(E, 0.6)
+        rep = P.pcgmg_solve(ops, b, cfg)
+        reps.append((rep, P.compliance(ops), P.mg_cycle(ops, np.zeros_like(f), f, gamma=gamma)))
+    (a, ca, va), (c, cc, vc) = reps
+    assert a.converged and a.iterations == c.iterations
+    assert a.residual_history == c.residual_history
+    assert np.array_equal(a.solution, c.solution) and ca == cc
+    assert np.array_equal(va, vc)
