@@ -58,7 +58,7 @@ struct TPlanes {
 
 template <bool UP>
 __global__ void __launch_bounds__(kTThreads) k_stile(const __grid_constant__ SMarchArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int W = t_side<UP>();
   constexpr int N = t_nodes<UP>();
   double* pl = reinterpret_cast<double*>(smem_raw);       // [19][W][W]
