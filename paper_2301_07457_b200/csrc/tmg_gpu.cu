@@ -1354,6 +1354,11 @@ void finish_update(H* h, int it) {
   });
 }
 
+// Lower half-bandwidth (in dofs) of the coarsest matrix: 2 dofs per node,
+// column-major node numbering, 9-point stencil (the lower neighbour farthest
+// away is (x-1, y-1), ny + 2 nodes back).
+int coarsest_band(const Grid& g0, int n) { return std::min(n - 1, 2 * (g0.ny + 2) + 1); }
+
 // dense Cholesky of the coarsest matrix, in shared memory when it fits
 void launch_cholesky(cudaStream_t s, double* A, int n, int* bad_row) {
   if (n <= kCholSmemMax) {
@@ -1414,7 +1419,14 @@ void setup(H* h, double omega) {
       k_dense_assemble<decltype(op)><<<dim3((g0.ny + 1 + 63) / 64, g0.nx + 1), 64, 0, h->stream>>>(op, g0, R->A0, n);
     });
     CKL();
-    launch_cholesky(h->stream, R->A0, n, R->bad_row);
+    const int b = coarsest_band(g0, n);
+    const size_t bsm = static_cast<size_t>(n) * (b + 1) * sizeof(double);
+    if (b <= 31 && bsm <= 200 * 1024) {
+      CK(cudaFuncSetAttribute(k_cholesky_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bsm)));
+      k_cholesky_band<<<1, 32, bsm, h->stream>>>(R->A0, n, b, R->bad_row);
+    } else {
+      launch_cholesky(h->stream, R->A0, n, R->bad_row);
+    }
     CKL();
     h->count(2);
   }
@@ -1432,7 +1444,8 @@ void setup(H* h, double omega) {
     const int wpb = 4;
     const size_t sm = sizeof(double) * n * wpb;
     CK(cudaFuncSetAttribute(k_lower_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-    k_lower_inverse<<<(n + wpb - 1) / wpb, 32 * wpb, sm, h->stream>>>(R->A0, R->LiT, n);
+    k_lower_inverse<<<(n + wpb - 1) / wpb, 32 * wpb, sm, h->stream>>>(R->A0, R->LiT, n,
+                                                                       coarsest_band(R->lev[0].g, n));
     CKL();
     k_gram<<<dim3((n + 127) / 128, n), 128, 0, h->stream>>>(R->LiT, R->Ainv, n);
     CKL();

@@ -515,8 +515,44 @@ __global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ Ag, int 
   const int t = threadIdx.x, nt = blockDim.x;
   const int lane = t & 31, w = t >> 5, nw = nt >> 5;
   double* A = SMEM ? As : Ag;
-  if (SMEM)
+  if (SMEM) {
+    // two barriers per column: every thread takes the pivot itself, and the
+    // scaled column is also staged contiguously (cv) so the trailing update
+    // reads it without the bank conflicts of the strided column
+    __shared__ double cv[kCholSmemMax];
     for (int k = t; k < n * n; k += nt) As[k] = Ag[k];
+    __syncthreads();
+    int bad = -1;
+    for (int k = 0; k < n; ++k) {
+      const double d = A[k * n + k];
+      if (!(d > 0.0)) {  // the same d in every thread: a uniform exit
+        bad = k;
+        break;
+      }
+      // only the threads that scale an entry (and thread 0, which stores the
+      // pivot) take the square root: a redundant DSQRT in all 1024 threads
+      // costs more FP64 issue than the barrier it saves
+      if (t == 0 || k + 1 + t < n) {
+        const double piv = sqrt(d);
+        for (int i = k + 1 + t; i < n; i += nt) {
+          const double l = A[i * n + k] / piv;
+          A[i * n + k] = l;
+          cv[i] = l;
+        }
+        if (t == 0) A[k * n + k] = piv;
+      }
+      __syncthreads();
+      for (int i = k + 1 + w; i < n; i += nw) {
+        const double lik = cv[i];
+        double* Ai = A + i * n;
+        for (int j = k + 1 + lane; j <= i; j += 32) Ai[j] -= lik * cv[j];
+      }
+      __syncthreads();
+    }
+    for (int k = t; k < n * n; k += nt) Ag[k] = As[k];
+    if (t == 0) *bad_row = bad;
+    return;
+  }
   if (t == 0) fail = -1;
   __syncthreads();
   for (int k = 0; k < n; ++k) {
@@ -544,9 +580,58 @@ __global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ Ag, int 
   if (t == 0) *bad_row = fail;
 }
 
+// Banded Cholesky of the coarsest matrix in one warp. With the column-major
+// node numbering the 9-point coarsest operator has lower half-bandwidth
+// b = 2 (ny + 2) + 1 dofs, and its factor has no fill outside the band (the
+// envelope the reference's CholeskyFactor exploits, solvers.cpp:89-148), so
+// only the band is staged in shared memory (Bs[i][d] = A[i][i-d]). Lane r
+// owns row k+1+r of step k and takes the other lanes' multipliers by
+// shuffles. Inside the band every entry sees the same operations in the same
+// order as in k_cholesky (outside it both leave exact zeros), so the factor
+// and the failing row are bitwise those of the dense kernel. b <= 31.
+__global__ void __launch_bounds__(32) k_cholesky_band(double* __restrict__ Ag, int n, int b, int* bad_row) {
+  extern __shared__ double Bs[];
+  const int lane = threadIdx.x, W = b + 1;
+  for (int e = lane; e < n * W; e += 32) {
+    const int i = e / W, d = e - i * W;
+    Bs[e] = (i - d >= 0) ? Ag[static_cast<long>(i) * n + i - d] : 0.0;
+  }
+  __syncwarp();
+  int bad = -1;
+  for (int k = 0; k < n; ++k) {
+    const double dk = Bs[k * W];
+    if (!(dk > 0.0)) {  // the same value in every lane: a uniform exit
+      bad = k;
+      break;
+    }
+    const double piv = sqrt(dk);
+    const int i = k + 1 + lane;
+    const bool valid = lane < b && i < n;
+    double l = 0.0;
+    if (valid) l = Bs[i * W + lane + 1] / piv;  // A[i][k]
+    __syncwarp();
+    if (valid) Bs[i * W + lane + 1] = l;
+    if (lane == 0) Bs[k * W] = piv;
+    // A[i][j] -= l_i l_j for k < j <= i, j = k + 1 + jj
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) {
+      const double lj = __shfl_sync(0xffffffffu, l, jj);
+      if (valid && jj <= lane) Bs[i * W + lane - jj] -= l * lj;
+    }
+    __syncwarp();
+  }
+  for (int e = lane; e < n * W; e += 32) {
+    const int i = e / W, d = e - i * W;
+    if (i - d >= 0) Ag[static_cast<long>(i) * n + i - d] = Bs[e];
+  }
+  if (lane == 0) *bad_row = bad;
+}
+
 // Column j of L^-1 (stored as row j of LiT), one warp per column, the
 // running column kept in shared memory.
-__global__ void k_lower_inverse(const double* __restrict__ L, double* __restrict__ LiT, int n) {
+// b: lower half-bandwidth of L (>= n - 1 when dense); with b <= 31 a row's
+// non-zeros left of the diagonal fit one 32-lane chunk.
+__global__ void k_lower_inverse(const double* __restrict__ L, double* __restrict__ LiT, int n, int b) {
   extern __shared__ double ycol[];
   const int wpb = blockDim.x >> 5;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -557,13 +642,66 @@ __global__ void k_lower_inverse(const double* __restrict__ L, double* __restrict
   __syncwarp();
   if (lane == 0) yv[j] = 1.0 / L[static_cast<long>(j) * n + j];
   __syncwarp();
-  for (int i = j + 1; i < n; ++i) {
-    const double* Li = L + static_cast<long>(i) * n;
-    double s = 0.0;
-    for (int k = j + lane; k < i; k += 32) s = fma(Li[k], yv[k], s);
-    s = warp_sum(s);
-    if (lane == 0) yv[i] = -s / Li[i];
-    __syncwarp();
+  if (b <= 31) {
+    // banded L: row i has non-zeros in columns [i - b, i]; one chunk per row,
+    // fetched one step ahead, the diagonal as a precomputed reciprocal
+    double cur = 0.0, nxt = 0.0, dcur = 0.0, dnxt = 0.0;
+    auto fetch = [&](int i, double& v, double& dg) {
+      const double* Li = L + static_cast<long>(i) * n;
+      const int k = max(j, i - b) + lane;
+      v = (k < i) ? Li[k] : 0.0;
+      dg = 1.0 / Li[i];
+    };
+    if (j + 1 < n) fetch(j + 1, cur, dcur);
+    for (int i = j + 1; i < n; ++i) {
+      if (i + 1 < n) fetch(i + 1, nxt, dnxt);
+      const int k = max(j, i - b) + lane;
+      double s = (k < i) ? cur * yv[k] : 0.0;
+      s = warp_sum(s);
+      if (lane == 0) yv[i] = -s * dcur;
+      __syncwarp();
+      cur = nxt;
+      dcur = dnxt;
+    }
+  } else if (n <= 192) {
+    // rows held in registers one step ahead: the L2 latency of row i+1
+    // overlaps the dependent reduction of row i (whose diagonal enters as a
+    // precomputed reciprocal)
+    double cur[6], nxt[6], dcur = 0.0, dnxt = 0.0;
+    auto fetch = [&](int i, double (&v)[6], double& dg) {
+      const double* Li = L + static_cast<long>(i) * n;
+#pragma unroll
+      for (int m = 0; m < 6; ++m) {
+        const int k = j + lane + 32 * m;
+        v[m] = (k < i) ? Li[k] : 0.0;
+      }
+      dg = 1.0 / Li[i];  // reciprocal of the diagonal, off the dependent chain
+    };
+    if (j + 1 < n) fetch(j + 1, cur, dcur);
+    for (int i = j + 1; i < n; ++i) {
+      if (i + 1 < n) fetch(i + 1, nxt, dnxt);
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < 6; ++m) {
+        const int k = j + lane + 32 * m;
+        if (k < i) s = fma(cur[m], yv[k], s);
+      }
+      s = warp_sum(s);
+      if (lane == 0) yv[i] = -s * dcur;
+      __syncwarp();
+#pragma unroll
+      for (int m = 0; m < 6; ++m) cur[m] = nxt[m];
+      dcur = dnxt;
+    }
+  } else {
+    for (int i = j + 1; i < n; ++i) {
+      const double* Li = L + static_cast<long>(i) * n;
+      double s = 0.0;
+      for (int k = j + lane; k < i; k += 32) s = fma(Li[k], yv[k], s);
+      s = warp_sum(s);
+      if (lane == 0) yv[i] = -s / Li[i];
+      __syncwarp();
+    }
   }
   for (int i = lane; i < n; i += 32) LiT[static_cast<long>(j) * n + i] = yv[i];
 }

@@ -455,7 +455,7 @@ void p_setup(PH* h, double omega) {
   const int wpb = 4;
   const size_t sm = sizeof(double) * n * wpb;
   CK(cudaFuncSetAttribute(k_lower_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-  k_lower_inverse<<<(n + wpb - 1) / wpb, 32 * wpb, sm, h->stream>>>(h->A0, h->LiT, n);
+  k_lower_inverse<<<(n + wpb - 1) / wpb, 32 * wpb, sm, h->stream>>>(h->A0, h->LiT, n, n);
   CKL();
   k_gram<<<dim3((n + 127) / 128, n), 128, 0, h->stream>>>(h->LiT, h->Ainv, n);
   CKL();
