@@ -357,6 +357,8 @@ struct tmg_gpu_handle {
   // scheme, conditional nodes on); the host launches it once per solve
   // (TMG_NO_DEVICE_LOOP=1 keeps the per-iteration host loop)
   bool device_loop = true;
+  // banded coarsest Cholesky (TMG_DENSE_COARSE_FACTOR=1: the dense kernel)
+  bool band_factor = true;
   cudaGraphExec_t loop = nullptr;
   long loop_first_kernels = 0, loop_head_kernels = 0, loop_rest_kernels = 0;
   int g_gamma = -1, g_pre = -1, g_post = -1;
@@ -1421,7 +1423,7 @@ void setup(H* h, double omega) {
     CKL();
     const int b = coarsest_band(g0, n);
     const size_t bsm = static_cast<size_t>(n) * (b + 1) * sizeof(double);
-    if (b <= 31 && bsm <= 200 * 1024) {
+    if (h->band_factor && b <= 31 && bsm <= 200 * 1024) {
       CK(cudaFuncSetAttribute(k_cholesky_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bsm)));
       k_cholesky_band<<<1, 32, bsm, h->stream>>>(R->A0, n, b, R->bad_row);
     } else {
@@ -1723,6 +1725,7 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
   if (const char* v = std::getenv("TMG_STILE_MAX_NODES")) hp->stile_max_nodes = std::atol(v);
   if (const char* v = std::getenv("TMG_NO_COND_NODES")) hp->cond_nodes = std::atoi(v) == 0;
   if (const char* v = std::getenv("TMG_NO_DEVICE_LOOP")) hp->device_loop = std::atoi(v) == 0;
+  if (const char* v = std::getenv("TMG_DENSE_COARSE_FACTOR")) hp->band_factor = std::atoi(v) == 0;
   for (cudaEvent_t& e : hp->ev) CK(cudaEventCreate(&e));
   for (int i = 0; i < nlocal; ++i) {
     hp->own.push_back(std::make_unique<Rank>());

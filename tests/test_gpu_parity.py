@@ -390,3 +390,27 @@ def test_tile_kernels_match_marching(monkeypatch, nx, ny, nc, recipe, gamma):
     assert a.residual_history == c.residual_history
     assert np.array_equal(a.solution, c.solution) and ca == cc
     assert np.array_equal(va, vc)
+
+
+@pytest.mark.parametrize("nx,ny,nc", [(64, 64, 3), (128, 96, 3), (160, 96, 4)])
+def test_banded_coarsest_factor_is_the_dense_one(monkeypatch, nx, ny, nc):
+    """The banded one-warp Cholesky of the coarsest matrix performs, inside
+    the band, the dense kernel's operations in the same order, so the solve is
+    bitwise the same as with the dense factor (TMG_DENSE_COARSE_FACTOR=1);
+    the singular (unsupported) structure fails at setup either way."""
+    _, E = moduli(nx, ny, "iid", 7)
+    g = P.GridLevel(nx, ny)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    b = P.assemble_rhs(g, bc)
+    reps = []
+    for dense in ("0", "1"):
+        monkeypatch.setenv("TMG_DENSE_COARSE_FACTOR", dense)
+        ops = P.MultigridOperators(g, nc, 0.3, bc)
+        ops.set_moduli(E, 0.6)
+        reps.append(P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-10, max_iter=300)))
+        free = P.MultigridOperators(P.GridLevel(8, 8), 2, 0.3, P.BoundaryConditions([], []))
+        with pytest.raises(P.DefinitenessError):
+            free.set_moduli(np.ones(64))
+    a, c = reps
+    assert a.iterations == c.iterations and a.residual_history == c.residual_history
+    assert np.array_equal(a.solution, c.solution)
