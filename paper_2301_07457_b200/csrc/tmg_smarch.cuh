@@ -44,9 +44,11 @@ constexpr int kSThreads = kSY + 32;     // + one producer warp
 template <bool UP>
 __host__ __device__ constexpr int s_stages() { return 6; }
 constexpr int kSRows = kSY + 2;         // streamed rows per column
-// every coarse level runs the two-stage kernels (measured on c1-c4: one-pass
-// kernels for the small levels were 1-13 % slower per PCG iteration); the
-// one-pass kernels remain for W-cycle revisits and other sweep counts
+// every coarse level runs the two-stage V(2,2) halves (measured on c1-c4:
+// one-pass kernels for the small levels were 1-13 % slower per PCG
+// iteration): these marching kernels above kTileMaxNodes, the shared-memory
+// tiles of tmg_stile.cuh below; the one-pass kernels remain for W-cycle
+// revisits and other sweep counts
 constexpr long kSMinNodes = 0;
 
 struct SMarchArgs {
