@@ -51,7 +51,18 @@ CONFIGS = {
            "c0 mesh: 64x64 Q4 wall, iid U(0,1) densities seed 0, 4 levels, tol 1e-8"),
     "c3": (1024, 1024, 7, "iid", 0,
            "c3 mesh: 1024x1024 Q4 wall, iid U(0,1) densities seed 0, 8 levels, tol 1e-8"),
+    # weak scaling: a (1024 N) x 8192 wall on N GPUs, 11 levels
+    "weak": (1024, 8192, 10, "iid", 1,
+             "weak: (1024 N)x8192 Q4 wall on N GPUs, iid U(0,1) densities seed 1, 11 levels, tol 1e-8"),
 }
+
+
+def config_of(name, ws):
+    """The CONFIGS entry, with the weak-scaling mesh widened to 1024 per GPU."""
+    nx, ny, nc, recipe, seed, desc = CONFIGS[name]
+    if name == "weak":
+        nx *= ws
+    return nx, ny, nc, recipe, seed, desc
 TOL, OMEGA, SWEEPS, MAX_ITER = 1e-8, 0.6, 2, 5000
 MATERIAL = dict(phase_moduli=[1.0, 0.5, 0.2, 1e-9], poisson_ratio=0.3, penalty=3.0)
 METRIC = "pCGMG MDOF/s (DOFs x PCG iterations / s, per solve incl. device setup)"
@@ -219,7 +230,7 @@ def reference_arm(args, cfg_name):
     from oracle import pyoracle as po
 
     kind = "ref" if po.available("ref") else "orc"
-    nx, ny, nc, recipe, seed, desc = CONFIGS[cfg_name]
+    nx, ny, nc, recipe, seed, desc = config_of(cfg_name, dist_env()[0])
     sx, sy, snc = CPU_SAMPLE
     job = (sx, sy, snc, recipe, seed, kind)
     pool = ReferencePool(host_cores())
@@ -268,7 +279,7 @@ def gpu_arm(args, cfg_name):
         uid = [P.nccl_unique_id() if rank == 0 else None]
         td.broadcast_object_list(uid, src=0)
         nccl = (ws, rank, uid[0])
-    nx, ny, nc, recipe, seed, desc = CONFIGS[cfg_name]
+    nx, ny, nc, recipe, seed, desc = config_of(cfg_name, dist_env()[0])
     g, bc, E, b = make_inputs(nx, ny, recipe, seed)
     dofs = g.dof_count()
     lib = P._lib.load()
@@ -361,20 +372,20 @@ def gpu_arm(args, cfg_name):
 
     result = None
     if rank == 0:
-        # strong scaling: the same global c4 solve at every N
+        # strong scaling: the same global solve at every N (weak: 1024 columns per GPU)
         value = dofs * sum(its) / (t_res * 1e-3) / 1e6
         e2e_value = dofs * sum(e_its) / (t_e2e * 1e-3) / 1e6
         result = {
             "metric": METRIC, "value": value, "unit": "MDOF/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_res / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if cfg_name == "weak" else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded densities with the BASELINE recipe; no dataset exists)",
             "config": {"workload": desc, "nx": nx, "ny": ny, "dofs": dofs, "levels": nc + 1, "tol": TOL,
                        "omega": OMEGA, "smoother": f"damped Jacobi {SWEEPS}+{SWEEPS}", "cycle": "V",
                        "pcg_iterations": its,
                        "parallelism": "single GPU" if ws == 1 else f"x-slab decomposition over {ws} GPUs (NCCL)",
                        "l2": "inputs larger than L2 (1.07 GB per fine vector); no flush needed"
-                       if cfg_name == "c4" else "working set partly L2-resident; no flush",
+                       if cfg_name in ("c4", "weak") else "working set partly L2-resident; no flush",
                        "solves_per_s": args.steps / (t_res * 1e-3),
                        "setup_ms_last": setup_ms, "pcg_ms_last": pcg_ms,
                        "pcg_only_mdof_s": dofs * its[-1] / (pcg_ms * 1e-3) / 1e6},
