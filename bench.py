@@ -184,6 +184,11 @@ def run_reference_sample(nx, ny, nc, recipe, seed, kind):
     return dofs * r["iterations"] / dt / 1e6, r["iterations"], dt
 
 
+def _ref_noop(sec):
+    time.sleep(sec)  # keeps each task on its own worker while the pool starts
+    return os.getpid()
+
+
 def _ref_worker(job):
     """One reference sample in a worker process (bench CPU leg only)."""
     _, it, dt = run_reference_sample(*job)
@@ -208,7 +213,10 @@ class ReferencePool:
         import multiprocessing as mp
 
         self.cores = cores
-        self.ex = cf.ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("fork"))
+        # spawn: the GPU arm forks nothing after CUDA and its threads are initialised
+        self.ex = cf.ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn"))
+        # start every worker (interpreter + imports) before anything is timed
+        list(self.ex.map(_ref_noop, [0.2] * cores))
 
     def step(self, job):
         """All cores run one sample; returns (MDOF*it/s aggregate, iterations, wall s)."""
