@@ -414,3 +414,32 @@ def test_banded_coarsest_factor_is_the_dense_one(monkeypatch, nx, ny, nc):
     a, c = reps
     assert a.iterations == c.iterations and a.residual_history == c.residual_history
     assert np.array_equal(a.solution, c.solution)
+
+
+def test_restrict_prolongate_known_answers():
+    """test_grid.cpp:106-137 on the device transfer kernels: zeros restrict to
+    zeros, and restrict(prolongate(spike)) is 0.5625 at the spike (the
+    hand-composed full-weighting stencil) with its maximum there."""
+    ops, _, _, _, _ = pair(8, 8, 1)
+    fine, coarse = ops.level(1), ops.level(0)
+    assert not np.any(ops.restrict(1, np.zeros(fine.dof_count())))
+    for comp in (0, 1):
+        c = np.zeros(coarse.dof_count())
+        spike = 2 * coarse.node_index(2, 2) + comp
+        c[spike] = 1.0
+        back = ops.restrict(1, ops.prolongate(1, c))
+        assert abs(back[spike] - 0.5625) <= 1e-14
+        assert np.argmax(back) == spike and np.sum(back == back[spike]) == 1
+
+
+def test_one_vcycle_contracts_poisson_residual():
+    """test_solvers.cpp:344-355: one V(2,2)-cycle from zero reduces the
+    Poisson residual (64^2, 5 coarsenings) by 5x or better; the device cycle
+    is measured under the checker's assembled matrix."""
+    g, nc = 64, 5
+    ops = P.PoissonMultigrid(P.GridLevel(g, g), nc)
+    sysc = po.poisson_system("orc", g, g, 1.0).build_mg(nc, 0.6)
+    b = sysc.rhs()
+    u = ops.vcycle(np.zeros_like(b), b, 1, 2, 2)
+    after = np.linalg.norm(b - sysc.matvec(nc, u))
+    assert after < 0.2 * np.linalg.norm(b)
