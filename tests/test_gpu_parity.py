@@ -443,3 +443,39 @@ def test_one_vcycle_contracts_poisson_residual():
     u = ops.vcycle(np.zeros_like(b), b, 1, 2, 2)
     after = np.linalg.norm(b - sysc.matvec(nc, u))
     assert after < 0.2 * np.linalg.norm(b)
+
+
+def test_device_sensitivities_known_answers():
+    """test_mto.cpp:72-114 on the device consumers: sensitivities vanish at
+    u = 0 and are never positive; the adjoint sensitivities match central
+    finite differences of the compliance of device solves (void modulus kept
+    finite so the difference stays above roundoff)."""
+    n, nc = 8, 2
+    mat = P.MaterialModel(phase_moduli=[9.0, 3.0, 1.0, 1e-3], poisson_ratio=0.3, penalty=3.0)
+    rng = np.random.default_rng(33)
+    a = rng.uniform(0.05, 1.0, (n * n, 4))
+    a /= a.sum(1, keepdims=True)
+    g = P.GridLevel(n, n)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    b = P.assemble_rhs(g, bc)
+    ops = P.MultigridOperators(g, nc, 0.3, bc)
+    cfg = P.SolverConfig(tol=1e-13, max_iter=500)
+
+    def compliance(alpha):
+        ops.set_moduli(P.effective_moduli(alpha, mat), 0.6)
+        rep = P.pcgmg_solve(ops, b, cfg)
+        assert rep.converged
+        return P.compliance(ops)
+
+    compliance(a)
+    assert not np.any(P.sensitivities(ops, a, mat, np.zeros(g.dof_count())))
+    assert np.all(P.sensitivities(ops, a, mat, rng.uniform(-1, 1, g.dof_count())) <= 0.0)
+    ad = P.sensitivities(ops, a, mat)  # at the resident solution
+    h = 1e-5
+    for e in range(0, n * n, 5):
+        for i in range(4):
+            up, dn = a.copy(), a.copy()
+            up[e, i] += h
+            dn[e, i] -= h
+            fd = (compliance(up) - compliance(dn)) / (2 * h)
+            assert abs(fd - ad[i, e]) <= 1e-3 * max(abs(ad[i, e]), 1e-12), (e, i, fd, ad[i, e])
