@@ -479,3 +479,21 @@ def test_device_sensitivities_known_answers():
             dn[e, i] -= h
             fd = (compliance(up) - compliance(dn)) / (2 * h)
             assert abs(fd - ad[i, e]) <= 1e-3 * max(abs(ad[i, e]), 1e-12), (e, i, fd, ad[i, e])
+
+
+def test_device_filter_known_answers():
+    """test_mto.cpp:116-135 on the device filter: radius <= 1 is the identity
+    (bitwise), and on a uniform design a uniform field stays uniform under a
+    radius-3 cone."""
+    n = 12
+    g = P.GridLevel(n, n)
+    ops = P.MultigridOperators(g, 2, 0.3, P.wall_boundary_conditions(g, "uniform"))
+    rng = np.random.default_rng(5)
+    a = rng.uniform(0.05, 1.0, (n * n, 4))
+    a /= a.sum(1, keepdims=True)
+    raw = -rng.uniform(0.0, 2.0, n * n)
+    assert np.array_equal(P.filter_sensitivities(ops, raw, a, 0, 1.0), raw)
+    assert np.array_equal(P.filter_sensitivities(ops, raw, a, 1, 0.5), raw)
+    uni = np.tile([0.3, 0.7], (n * n, 1))  # DensityField::uniform(8, 8, {0.3, 0.7}) of the reference test
+    f = P.filter_sensitivities(ops, np.full(n * n, -1.75), uni, 0, 3.0)
+    np.testing.assert_allclose(f, -1.75, rtol=1e-13)
