@@ -146,9 +146,11 @@ def test_reference_itself_when_available():
     assert rel(rep.solution, ref["solution"]) <= 1e-8
 
 
-def test_tight_tolerance_matches_direct_solution():
-    """acceptance.cpp:156-190: pCGMG at tol 1e-10 within 1e-8 of Cholesky."""
-    ops, sysc, b, _, _ = pair(32, 32, 2, recipe="uniform")
+@pytest.mark.parametrize("n,nc,recipe", [(16, 1, "uniform"), (32, 2, "uniform"), (64, 3, "iid"), (64, 3, "checker")])
+def test_tight_tolerance_matches_direct_solution(n, nc, recipe):
+    """acceptance.cpp:156-190: pCGMG at tol 1e-10 within 1e-8 of the direct
+    solution (the checker's CG to 1e-14) on elasticity 16/32/64."""
+    ops, sysc, b, _, _ = pair(n, n, nc, recipe=recipe)
     rep = P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-10, max_iter=2000))
     tight = sysc.solve(b, tol=1e-14, max_iter=5000)
     assert rel(rep.solution, tight["solution"]) <= 1e-8
