@@ -68,6 +68,9 @@ MATERIAL = dict(phase_moduli=[1.0, 0.5, 0.2, 1e-9], poisson_ratio=0.3, penalty=3
 METRIC = "pCGMG MDOF/s (DOFs x PCG iterations / s, per solve incl. device setup)"
 # bounded CPU sample (same recipe as the workload, 512x512, one full solve)
 CPU_SAMPLE = (512, 512, 6)
+SAMPLE_WHY = ("the reference cannot run c4 itself: its CSR row offsets are int (sparse.hpp:53, sparse.cpp:44-45) "
+              "and 8192^2 needs ~2.42e9 nonzeros > INT_MAX, plus >100 GB of assembly triplets; a 512^2 solve of "
+              "the same recipe is ~5 s of single-threaded work, one per host core")
 
 
 def dist_env():
@@ -173,14 +176,21 @@ def run_reference_sample(nx, ny, nc, recipe, seed, kind):
     pcgmg_solve) on the host, 1 thread; returns (MDOF*it/s, iterations, s)."""
     from oracle import pyoracle as po  # CPU checker / reference -- bench CPU leg only
 
-    g, bc, E, b = make_inputs(nx, ny, recipe, seed)
+    # inputs through the reference side only (its oracle::Rng recipe and its
+    # effective_moduli; nothing of the product library is loaded here)
+    if recipe == "iid":
+        alpha = po.density_iid(kind, nx, ny, seed)
+    else:
+        alpha = po.density_checker(kind, nx, ny, 16, seed)
+    E = po.effective_moduli(kind, nx, ny, alpha, MATERIAL["phase_moduli"], MATERIAL["penalty"])
+    fixed, loads = po.wall_uniform_bc(nx, ny)
     t0 = time.perf_counter()
-    s = po.System(kind, nx, ny, E, MATERIAL["poisson_ratio"], bc.fixed_dofs, bc.point_loads)
+    s = po.System(kind, nx, ny, E, MATERIAL["poisson_ratio"], fixed, loads)
     s.build_mg(nc, OMEGA)
     r = s.solve(s.rhs(), tol=TOL, max_iter=MAX_ITER, gamma=1, pre=SWEEPS, post=SWEEPS)
     dt = time.perf_counter() - t0
     s.close()
-    dofs = g.dof_count()
+    dofs = 2 * (nx + 1) * (ny + 1)
     return dofs * r["iterations"] / dt / 1e6, r["iterations"], dt
 
 
@@ -262,7 +272,9 @@ def reference_arm(args, cfg_name):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": desc, "sample": f"{sx}x{sy}", "samples_per_step": pool.cores,
-                                         "pcg_iterations_per_step": its},
+                                         "pcg_iterations_per_step": its, "why_sample": SAMPLE_WHY,
+                                         "inputs": "generated by oracle/_ref (the reference's oracle::Rng recipe "
+                                                   "and effective_moduli); the product library is not loaded"},
         "cpu_baseline": {"value": value, "unit": "MDOF/s", "cores": pool.cores,
                          "kind": "reference" if kind == "ref" else "port", "sample": sample},
         "e2e": {"value": value, "unit": "MDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -284,6 +296,8 @@ def gpu_arm(args, cfg_name):
 
         td.init_process_group("gloo")
         dist = td
+        print(f"[bench] rank {rank}/{ws} (local {local}): control plane up, NCCL solver communicator next",
+              file=sys.stderr, flush=True)
         uid = [P.nccl_unique_id() if rank == 0 else None]
         td.broadcast_object_list(uid, src=0)
         nccl = (ws, rank, uid[0])
@@ -427,7 +441,7 @@ def gpu_arm(args, cfg_name):
                 "sample": f"{sx}x{sy} mesh, {recipe} seed {seed}, {snc + 1} levels: {pool.cores} concurrent "
                           f"single-threaded samples (the reference has no threading; one per host core), each "
                           f"one full assemble + build_multigrid_operators + pcgmg_solve ({it} PCG iterations in "
-                          f"total, {dt:.1f} s wall)"}
+                          f"total, {dt:.1f} s wall); {SAMPLE_WHY}"}
     lib.tmg_host_free(C.c_void_p(pE))
     lib.tmg_host_free(C.c_void_p(pb))
     lib.tmg_host_free(C.c_void_p(px))
@@ -439,6 +453,25 @@ def gpu_arm(args, cfg_name):
     return 0
 
 
+def free_port():
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launch_ranks(n):
+    """--gpus N without a torchrun environment: start N ranks (one process per
+    GPU) through torch.distributed.run on 127.0.0.1 and return its exit code;
+    rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", str(pathlib.Path(__file__).resolve()),
+           *sys.argv[1:]]
+    print(f"[bench] launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -448,6 +481,11 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return launch_ranks(args.gpus)
+    ws = dist_env()[0]
+    if ws != args.gpus:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={ws}: running {ws} ranks", file=sys.stderr, flush=True)
     if args.impl == "reference":
         return reference_arm(args, args.config)
     return gpu_arm(args, args.config)

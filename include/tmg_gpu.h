@@ -268,9 +268,12 @@ void tmg_inputs_density_checker(int nx, int ny, int block, int nphases,
                                 unsigned long long seed, double* alpha);
 void tmg_inputs_wall_bc(int nx, int ny, int load_mode, int* fixed, int* n_fixed,
                         int* load_dofs, double* load_vals, int* n_loads);
-void tmg_inputs_rhs(int nx, int ny, const int* fixed, int n_fixed,
-                    const int* load_dofs, const double* load_vals, int n_loads,
-                    double* b);
+/* BoundaryConditions::validate (fem.cpp:110-129) + the rhs of
+ * assemble_from_moduli (fem.cpp:214-218): TMG_ERR_CONFIG for a dof outside
+ * [0, 2(nx+1)(ny+1)) or a dof both fixed and loaded (b untouched) */
+int tmg_inputs_rhs(int nx, int ny, const int* fixed, int n_fixed,
+                   const int* load_dofs, const double* load_vals, int n_loads,
+                   double* b);
 /* poisson_element_matrix / poisson_mass_matrix (fem.cpp:37-81), row-major 4x4 */
 void tmg_poisson_element_matrices(double* k16, double* m16);
 /* the right-hand side of assemble_poisson (fem.cpp:243-276) for a per-node

@@ -64,6 +64,7 @@ class PcgmgGpu {
   }
   // effective_moduli on the device (density.cpp:68-85), then set_moduli
   void set_density(const DensityField& d, const MaterialModel& mat, double omega) {
+    check_density(d, mat, "set_density");
     check(tmg_gpu_set_density(h_, d.values().data(), d.num_phases(), mat.phase_moduli.data(), mat.penalty,
                               omega));
   }
@@ -73,6 +74,10 @@ class PcgmgGpu {
                     const std::vector<double>* x0 = nullptr) {
     if (static_cast<int>(b.size()) != grid_.dof_count())
       throw DimensionError("pcgmg_solve: rhs length does not match the grid");
+    // r = b - A x0 (solvers.cpp:346-350) checks x0 through the matvec (sparse.cpp:72-75)
+    if (x0 && x0->size() != b.size())
+      throw DimensionError("matvec: vector length " + std::to_string(x0->size()) + " does not match matrix size " +
+                           std::to_string(b.size()));
     SolveReport rep;
     rep.solution.resize(b.size());
     rep.residual_history.resize(static_cast<size_t>(cfg.max_iter) + 1);
@@ -100,6 +105,7 @@ class PcgmgGpu {
   }
   // sensitivities (mto.cpp:61-85) of the resident solution
   std::vector<std::vector<double>> sensitivities(const DensityField& d, const MaterialModel& mat) const {
+    check_density(d, mat, "sensitivities");  // mto.cpp:65-70
     const size_t ne = static_cast<size_t>(grid_.element_count());
     std::vector<double> flat(ne * static_cast<size_t>(d.num_phases()));
     check(tmg_gpu_sensitivities(h_, nullptr, d.num_phases(), d.values().data(), mat.phase_moduli.data(),
@@ -111,6 +117,10 @@ class PcgmgGpu {
   // filter_sensitivities (mto.cpp:87-117)
   std::vector<double> filter_sensitivities(const std::vector<double>& raw, const DensityField& d, int phase,
                                            double radius) const {
+    if (static_cast<int>(raw.size()) != grid_.element_count())  // mto.cpp:90-92
+      throw DimensionError("filter: field length does not match element count");
+    if (radius > 1.0 && (d.nx() != grid_.nx || d.ny() != grid_.ny))
+      throw DimensionError("filter: density grid does not match level");
     std::vector<double> out(raw.size());
     check(tmg_gpu_filter(h_, d.num_phases(), d.values().data(), phase, radius, raw.data(), out.data()));
     return out;
@@ -121,6 +131,8 @@ class PcgmgGpu {
                       const std::vector<double>& filtered_sens_b, double target_fraction,
                       const std::vector<double>& move, double damping) const {
     const size_t ne = static_cast<size_t>(d.element_count());
+    if (d.nx() != grid_.nx || d.ny() != grid_.ny)
+      throw DimensionError("oc_update_pair: density grid does not match the handle's grid");
     if (phase_a == phase_b) throw ConfigError("oc_update_pair: phases must differ");
     if (filtered_sens_a.size() != ne || filtered_sens_b.size() != ne || move.size() != ne)
       throw DimensionError("oc_update_pair: field length does not match grid");
@@ -152,6 +164,13 @@ class PcgmgGpu {
       h_ = nullptr;
       throw;
     }
+  }
+  // sensitivities' checks (mto.cpp:65-70), applied wherever a density
+  // crosses the boundary
+  void check_density(const DensityField& d, const MaterialModel& mat, const char* what) const {
+    if (d.nx() != grid_.nx || d.ny() != grid_.ny)
+      throw DimensionError(std::string(what) + ": density grid does not match level");
+    if (d.num_phases() != mat.num_phases()) throw DimensionError(std::string(what) + ": phase count mismatch");
   }
   void check(int st) const {
     if (st != TMG_OK) throw_status(st, h_);

@@ -71,6 +71,8 @@ def lib(kind: str):
         "system_destroy": (None, [C.c_void_p]),
         "element_energies": (C.c_int, [C.c_int, C.c_int, _D, C.c_double, _D]),
         "effective_moduli": (None, [C.c_int, C.c_int, C.c_int, _D, _D, C.c_double, _D]),
+        "density_iid": (None, [C.c_int, C.c_int, C.c_int, C.c_ulonglong, _D]),
+        "density_checker": (None, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_ulonglong, _D]),
         "sensitivities": (C.c_int, [C.c_int, C.c_int, C.c_int, _D, _D, C.c_double, C.c_double, _D, _D]),
         "filter": (C.c_int, [C.c_int, C.c_int, C.c_int, _D, C.c_int, C.c_double, _D, _D]),
     }
@@ -80,6 +82,38 @@ def lib(kind: str):
         f.argtypes = args
     _cache[kind] = L
     return L
+
+
+def density_iid(kind, nx, ny, seed, nmat=3):
+    """BASELINE c1/c4 densities [nx*ny, nmat+1] (oracles.hpp:21-23 recipe)."""
+    a = np.empty((nx * ny, nmat + 1))
+    getattr(lib(kind), kind + "_density_iid")(nx, ny, nmat, seed, _d(a))
+    return a
+
+
+def density_checker(kind, nx, ny, block, seed, nphases=4):
+    """BASELINE c2 one-hot checkerboard [nx*ny, nphases]."""
+    a = np.empty((nx * ny, nphases))
+    getattr(lib(kind), kind + "_density_checker")(nx, ny, block, nphases, seed, _d(a))
+    return a
+
+
+def effective_moduli(kind, nx, ny, alpha, phase_moduli, penalty):
+    """effective_moduli (density.cpp:68-85)."""
+    a = np.ascontiguousarray(alpha, dtype=np.float64)
+    pm = np.ascontiguousarray(phase_moduli, dtype=np.float64)
+    out = np.empty(nx * ny)
+    getattr(lib(kind), kind + "_effective_moduli")(nx, ny, a.shape[1], _d(a), _d(pm), penalty, _d(out))
+    return out
+
+
+def wall_uniform_bc(nx, ny):
+    """BASELINE supports and load: both dofs of every bottom
+    node fixed (fem.cpp:328-332), -1/(nx+1) on the v-dof of every top node."""
+    x = np.arange(nx + 1)
+    fixed = np.stack([2 * x * (ny + 1), 2 * x * (ny + 1) + 1], axis=1).ravel().tolist()
+    loads = [(int(2 * (xi * (ny + 1) + ny) + 1), -1.0 / (nx + 1)) for xi in x]
+    return fixed, loads
 
 
 class System:

@@ -28,6 +28,9 @@
 #include "topmg/report.hpp"
 #include "topmg/solvers.hpp"
 #include "topmg/sparse.hpp"
+// the reference test suite's deterministic generator (tests/oracles.hpp:15-36):
+// its bit recipe defines the BASELINE densities
+#include "oracles.hpp"
 
 namespace {
 
@@ -284,6 +287,43 @@ topmg::DensityField make_density(int nx, int ny, int nphases, const double* alph
   return d;
 }
 }  // namespace
+
+// BASELINE c1/c4 densities drawn with the reference's own
+// oracle::Rng (oracles.hpp:21-23): element-major, nmat fractions U(0,1) per
+// element, divided by their sum when it exceeds 1, void = remainder.
+void ref_density_iid(int nx, int ny, int nmat, unsigned long long seed, double* alpha) {
+  oracle::Rng rng(seed);
+  const long ne = static_cast<long>(nx) * ny;
+  for (long e = 0; e < ne; ++e) {
+    double* a = alpha + e * (nmat + 1);
+    double s = 0.0;
+    for (int m = 0; m < nmat; ++m) {
+      a[m] = rng.uniform();
+      s += a[m];
+    }
+    if (s > 1.0) {
+      for (int m = 0; m < nmat; ++m) a[m] /= s;
+      s = 0.0;
+      for (int m = 0; m < nmat; ++m) s += a[m];
+    }
+    const double v = 1.0 - s;
+    a[nmat] = v > 0.0 ? v : 0.0;
+  }
+}
+
+// BASELINE c2 checkerboard: block x block element tiles visited x-major, one
+// phase per tile from oracle::Rng::index (oracles.hpp:24), one-hot alpha.
+void ref_density_checker(int nx, int ny, int block, int nphases, unsigned long long seed, double* alpha) {
+  oracle::Rng rng(seed);
+  std::memset(alpha, 0, sizeof(double) * static_cast<std::size_t>(nx) * ny * nphases);
+  for (int i = 0; i < (nx + block - 1) / block; ++i)
+    for (int j = 0; j < (ny + block - 1) / block; ++j) {
+      const int ph = rng.index(nphases);
+      for (int ex = i * block; ex < nx && ex < (i + 1) * block; ++ex)
+        for (int ey = j * block; ey < ny && ey < (j + 1) * block; ++ey)
+          alpha[(static_cast<long>(ex) * ny + ey) * nphases + ph] = 1.0;
+    }
+}
 
 void ref_effective_moduli(int nx, int ny, int nphases, const double* alpha,
                           const double* phase_moduli, double penalty, double* out) {

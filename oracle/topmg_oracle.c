@@ -9,6 +9,7 @@
 #include "topmg_oracle.h"
 
 #include <math.h>
+#include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -737,6 +738,82 @@ int orc_element_energies(int nx, int ny, const double* u, double nu, double* out
 }
 
 /* E_e = sum_i alpha_i^p E_i: density.cpp:68-85 */
+/* std::mt19937_64 (the generator of the reference's oracle::Rng,
+ * tests/oracles.hpp:15-36) restated in C: the standard's 64-bit Mersenne
+ * twister parameters, seeded by the standard's recurrence. */
+typedef struct {
+  uint64_t mt[312];
+  int idx;
+} Mt64;
+
+static void mt64_seed(Mt64* g, uint64_t seed) {
+  g->mt[0] = seed;
+  for (int i = 1; i < 312; ++i)
+    g->mt[i] = 6364136223846793005ULL * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+  g->idx = 312;
+}
+
+static uint64_t mt64_next(Mt64* g) {
+  if (g->idx >= 312) {
+    for (int i = 0; i < 312; ++i) {
+      const uint64_t x = (g->mt[i] & 0xFFFFFFFF80000000ULL) | (g->mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+      uint64_t xa = x >> 1;
+      if (x & 1) xa ^= 0xB5026F5AA96619E9ULL;
+      g->mt[i] = g->mt[(i + 156) % 312] ^ xa;
+    }
+    g->idx = 0;
+  }
+  uint64_t y = g->mt[g->idx++];
+  y ^= (y >> 29) & 0x5555555555555555ULL;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+  y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+  y ^= y >> 43;
+  return y;
+}
+
+/* oracle::Rng::uniform (oracles.hpp:21-23) */
+static double mt64_uniform(Mt64* g) { return (double)(mt64_next(g) >> 11) * 0x1.0p-53; }
+
+/* BASELINE c1/c4 densities: element-major, nmat fractions
+ * U(0,1), divided by their sum when it exceeds 1, void = remainder */
+void orc_density_iid(int nx, int ny, int nmat, unsigned long long seed, double* alpha) {
+  Mt64* g = (Mt64*)malloc(sizeof(Mt64));
+  mt64_seed(g, seed);
+  const long ne = (long)nx * ny;
+  for (long e = 0; e < ne; ++e) {
+    double* a = alpha + e * (nmat + 1);
+    double s = 0.0;
+    for (int m = 0; m < nmat; ++m) {
+      a[m] = mt64_uniform(g);
+      s += a[m];
+    }
+    if (s > 1.0) {
+      for (int m = 0; m < nmat; ++m) a[m] /= s;
+      s = 0.0;
+      for (int m = 0; m < nmat; ++m) s += a[m];
+    }
+    const double v = 1.0 - s;
+    a[nmat] = v > 0.0 ? v : 0.0;
+  }
+  free(g);
+}
+
+/* BASELINE c2 checkerboard: one phase per block x block tile (x-major,
+ * oracle::Rng::index, oracles.hpp:24), one-hot */
+void orc_density_checker(int nx, int ny, int block, int nphases, unsigned long long seed, double* alpha) {
+  Mt64* g = (Mt64*)malloc(sizeof(Mt64));
+  mt64_seed(g, seed);
+  memset(alpha, 0, sizeof(double) * (size_t)nx * ny * nphases);
+  for (int i = 0; i < (nx + block - 1) / block; ++i)
+    for (int j = 0; j < (ny + block - 1) / block; ++j) {
+      const int ph = (int)(mt64_next(g) % (uint64_t)nphases);
+      for (int ex = i * block; ex < nx && ex < (i + 1) * block; ++ex)
+        for (int ey = j * block; ey < ny && ey < (j + 1) * block; ++ey)
+          alpha[((long)ex * ny + ey) * nphases + ph] = 1.0;
+    }
+  free(g);
+}
+
 void orc_effective_moduli(int nx, int ny, int np, const double* alpha,
                           const double* pm, double pen, double* out) {
   const long ne = (long)nx * ny;

@@ -59,6 +59,11 @@ void orc_system_destroy(void* h);
 
 /* fem.cpp:292-318 */
 int orc_element_energies(int nx, int ny, const double* u, double nu, double* out);
+/* BASELINE densities with the reference's oracle::Rng recipe
+ * (tests/oracles.hpp:15-36): iid fractions and the c2
+ * checkerboard, element-major [nx*ny][nphases] */
+void orc_density_iid(int nx, int ny, int nmat, unsigned long long seed, double* alpha);
+void orc_density_checker(int nx, int ny, int block, int nphases, unsigned long long seed, double* alpha);
 /* density.cpp:68-85 */
 void orc_effective_moduli(int nx, int ny, int nphases, const double* alpha,
                           const double* phase_moduli, double penalty, double* out);

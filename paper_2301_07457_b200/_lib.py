@@ -93,7 +93,7 @@ SIGNATURES = [
     ("tmg_inputs_density_iid", None, [C.c_int, C.c_int, C.c_int, C.c_ulonglong, _D]),
     ("tmg_inputs_density_checker", None, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_ulonglong, _D]),
     ("tmg_inputs_wall_bc", None, [C.c_int, C.c_int, C.c_int, _I, _I, _I, _D, _I]),
-    ("tmg_inputs_rhs", None, [C.c_int, C.c_int, _I, C.c_int, _I, _D, C.c_int, _D]),
+    ("tmg_inputs_rhs", C.c_int, [C.c_int, C.c_int, _I, C.c_int, _I, _D, C.c_int, _D]),
 ]
 
 _lib = None

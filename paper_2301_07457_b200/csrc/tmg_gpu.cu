@@ -362,6 +362,10 @@ struct tmg_gpu_handle {
   cudaGraphExec_t loop = nullptr;
   long loop_first_kernels = 0, loop_head_kernels = 0, loop_rest_kernels = 0;
   int g_gamma = -1, g_pre = -1, g_post = -1;
+  // omega the graphs were captured with: it is a by-value kernel argument
+  // (fixed when the operators are built, solvers.cpp:471), so a setup with a
+  // new omega re-captures
+  double g_omega = -1.0;
   bool g_fused = false;
   // node columns per tile of the fine-level reductions (red_tiles)
   int red_tx = 64;
@@ -1261,7 +1265,7 @@ void capture_loop(H* h, int gamma, int pre, int post) {
 // Two graphs alternate the roles of the two direction buffers, because the
 // fused p-update reads the old p around each node while writing the new one.
 void capture_iteration(H* h, int gamma, int pre, int post) {
-  if (h->graph[0] && h->g_gamma == gamma && h->g_pre == pre && h->g_post == post) return;
+  if (h->graph[0] && h->g_gamma == gamma && h->g_pre == pre && h->g_post == post && h->g_omega == h->omega) return;
   for (auto& gx : h->graph) {
     if (gx) cudaGraphExecDestroy(gx);
     gx = nullptr;
@@ -1339,6 +1343,7 @@ void capture_iteration(H* h, int gamma, int pre, int post) {
   h->g_gamma = gamma;
   h->g_pre = pre;
   h->g_post = post;
+  h->g_omega = h->omega;
   h->g_fused = fused_upd;
 }
 

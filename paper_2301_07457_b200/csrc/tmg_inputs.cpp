@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <vector>
 #include <random>
 
 #include "../../include/tmg_gpu.h"
@@ -149,12 +150,23 @@ void tmg_inputs_wall_bc(int nx, int ny, int load_mode, int* fixed, int* n_fixed,
 }
 
 // rhs of the eliminated system: loads summed in order, fixed entries zeroed.
-void tmg_inputs_rhs(int nx, int ny, const int* fixed, int n_fixed, const int* load_dofs,
-                    const double* load_vals, int n_loads, double* b) {
+// BoundaryConditions::validate first (fem.cpp:110-129): a fixed or loaded dof
+// outside [0, n) or a dof both fixed and loaded returns TMG_ERR_CONFIG and
+// leaves b untouched.
+int tmg_inputs_rhs(int nx, int ny, const int* fixed, int n_fixed, const int* load_dofs,
+                   const double* load_vals, int n_loads, double* b) {
   const long n = 2L * (nx + 1) * (ny + 1);
+  std::vector<char> is_fixed(static_cast<size_t>(n), 0);
+  for (int i = 0; i < n_fixed; ++i) {
+    if (fixed[i] < 0 || fixed[i] >= n) return 1;
+    is_fixed[static_cast<size_t>(fixed[i])] = 1;
+  }
+  for (int i = 0; i < n_loads; ++i)
+    if (load_dofs[i] < 0 || load_dofs[i] >= n || is_fixed[static_cast<size_t>(load_dofs[i])]) return 1;
   std::memset(b, 0, sizeof(double) * static_cast<size_t>(n));
   for (int i = 0; i < n_loads; ++i) b[load_dofs[i]] += load_vals[i];
   for (int i = 0; i < n_fixed; ++i) b[fixed[i]] = 0.0;
+  return 0;
 }
 
 // poisson_element_matrix / poisson_mass_matrix (fem.cpp:37-81): 2x2 Gauss

@@ -215,14 +215,45 @@ def wall_boundary_conditions(grid: GridLevel, load: str = "point") -> BoundaryCo
                               point_loads=list(zip(ld[: nl.value].tolist(), lv[: nl.value].tolist())))
 
 
+def validate_boundary_conditions(bc: BoundaryConditions, dof_count: int) -> None:
+    """BoundaryConditions::validate (fem.cpp:110-129), message for message."""
+    is_fixed = np.zeros(dof_count, dtype=bool)
+    for d in bc.fixed_dofs:
+        if d < 0 or d >= dof_count:
+            raise ConfigError(f"fixed dof {d} outside [0, {dof_count})")
+        is_fixed[d] = True
+    for d, _ in bc.point_loads:
+        if d < 0 or d >= dof_count:
+            raise ConfigError(f"loaded dof {d} outside [0, {dof_count})")
+        if is_fixed[d]:
+            raise ConfigError(f"dof {d} is both fixed and loaded")
+
+
 def assemble_rhs(grid: GridLevel, bc: BoundaryConditions) -> np.ndarray:
-    """rhs of assemble_from_moduli: loads summed, fixed entries zeroed."""
+    """rhs of assemble_from_moduli: loads summed, fixed entries zeroed
+    (fem.cpp:214-218), after BoundaryConditions::validate."""
+    validate_boundary_conditions(bc, grid.dof_count())
     fixed = np.ascontiguousarray(bc.fixed_dofs, dtype=np.int32)
     ld = np.ascontiguousarray([d for d, _ in bc.point_loads], dtype=np.int32)
     lv = np.ascontiguousarray([v for _, v in bc.point_loads], dtype=np.float64)
     b = np.empty(grid.dof_count())
-    _lib.load().tmg_inputs_rhs(grid.nx, grid.ny, iptr(fixed), len(fixed), iptr(ld), dptr(lv), len(lv), dptr(b))
+    st = _lib.load().tmg_inputs_rhs(grid.nx, grid.ny, iptr(fixed), len(fixed), iptr(ld), dptr(lv), len(lv),
+                                    dptr(b))
+    if st != 0:
+        raise ConfigError("invalid boundary conditions")
     return b
+
+
+def _check_dofs(what: str, v: np.ndarray | None, n: int, fmt: str):
+    if v is not None and v.size != n:
+        raise DimensionError(fmt.format(what=what, got=v.size, n=n))
+
+
+def _check_density(alpha: np.ndarray, grid: GridLevel, nphases: int | None, what: str):
+    if alpha.ndim != 2 or alpha.shape[0] != grid.element_count():
+        raise DimensionError(f"{what}: density grid does not match level")
+    if nphases is not None and alpha.shape[1] != nphases:
+        raise DimensionError(f"{what}: phase count mismatch")
 
 
 # ------------------------------------------------------------- GPU solver --
@@ -408,6 +439,8 @@ def pcgmg_solve(ops: MultigridOperators, b: np.ndarray, cfg: SolverConfig,
     if b.size != ops.grid.dof_count():
         raise DimensionError(f"rhs length {b.size} != dof count {ops.grid.dof_count()}")
     x0c = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+    # r = b - A x0 (solvers.cpp:346-350): the reference's matvec length check
+    _check_dofs("matvec", x0c, b.size, "{what}: vector length {got} does not match matrix size {n}")
     x = np.empty_like(b)
     it = C.c_int()
     fr = C.c_double()
@@ -425,6 +458,7 @@ def pcgmg_solve(ops: MultigridOperators, b: np.ndarray, cfg: SolverConfig,
 def compliance(ops: MultigridOperators, u: np.ndarray | None = None) -> float:
     """u^T K u (fem.cpp:284-290); u=None uses the resident solution."""
     uc = None if u is None else np.ascontiguousarray(u, dtype=np.float64)
+    _check_dofs("compliance", uc, ops.grid.dof_count(), "{what}: vector length {got} != matrix size {n}")
     out = C.c_double()
     ops._check(ops.lib.tmg_gpu_compliance(ops.h, dptr(uc), C.byref(out)))
     return out.value
@@ -432,6 +466,7 @@ def compliance(ops: MultigridOperators, u: np.ndarray | None = None) -> float:
 
 def element_energies(ops: MultigridOperators, u: np.ndarray | None = None) -> np.ndarray:
     uc = None if u is None else np.ascontiguousarray(u, dtype=np.float64)
+    _check_dofs("element_energies", uc, ops.grid.dof_count(), "{what}: vector length {got} != dof count {n}")
     out = np.empty(ops.grid.element_count())
     ops._check(ops.lib.tmg_gpu_element_energies(ops.h, dptr(uc), dptr(out)))
     return out
@@ -443,6 +478,9 @@ def sensitivities(ops: MultigridOperators, alpha: np.ndarray, material: Material
     uc = None if u is None else np.ascontiguousarray(u, dtype=np.float64)
     a = np.ascontiguousarray(alpha, dtype=np.float64)
     pm = np.ascontiguousarray(material.phase_moduli, dtype=np.float64)
+    # mto.cpp:65-70, then element_energies' length check (fem.cpp:295-298)
+    _check_density(a, ops.grid, pm.size, "sensitivities")
+    _check_dofs("element_energies", uc, ops.grid.dof_count(), "{what}: vector length {got} != dof count {n}")
     out = np.empty((a.shape[1], a.shape[0]))
     ops._check(ops.lib.tmg_gpu_sensitivities(ops.h, dptr(uc), a.shape[1], dptr(a), dptr(pm),
                                              material.penalty, dptr(out)))
@@ -456,6 +494,8 @@ def filter_sensitivities(ops: MultigridOperators, raw: np.ndarray, alpha: np.nda
     a = np.ascontiguousarray(alpha, dtype=np.float64)
     if r.size != ops.grid.element_count():
         raise DimensionError("filter: field length does not match element count")
+    if radius > 1.0:  # the density is read only then (mto.cpp:93)
+        _check_density(a, ops.grid, None, "filter")
     out = np.empty_like(r)
     ops._check(ops.lib.tmg_gpu_filter(ops.h, a.shape[1], dptr(a), phase, radius, dptr(r), dptr(out)))
     return out

@@ -112,3 +112,53 @@ def test_config_errors_precede_device_work():
         P.MultigridOperators(P.GridLevel(10, 8), 2, 0.3, P.BoundaryConditions())
     with pytest.raises(P.ConfigError):
         P.MultigridOperators(P.GridLevel(0, 8), 0, 0.3, P.BoundaryConditions())
+
+
+def test_boundary_condition_validation_mirrors_reference():
+    """BoundaryConditions::validate (fem.cpp:110-129), in the Python mirror and
+    in the C entry point itself (which leaves b untouched)."""
+    g = P.GridLevel(4, 4)
+    n = g.dof_count()
+    cases = [
+        (P.BoundaryConditions([n], []), f"fixed dof {n} outside [0, {n})"),
+        (P.BoundaryConditions([-1], []), f"fixed dof -1 outside [0, {n})"),
+        (P.BoundaryConditions([0], [(n + 3, 1.0)]), f"loaded dof {n + 3} outside [0, {n})"),
+        (P.BoundaryConditions([0, 7], [(7, -1.0)]), "dof 7 is both fixed and loaded"),
+    ]
+    lib = P._lib.load()
+    for bc, msg in cases:
+        with pytest.raises(P.ConfigError, match=msg.replace("[", r"\[").replace("(", r"\(").replace(")", r"\)")):
+            P.assemble_rhs(g, bc)
+        fixed = np.ascontiguousarray(bc.fixed_dofs, dtype=np.int32)
+        ld = np.ascontiguousarray([d for d, _ in bc.point_loads], dtype=np.int32)
+        lv = np.ascontiguousarray([v for _, v in bc.point_loads], dtype=np.float64)
+        b = np.full(n, 7.0)
+        from paper_2301_07457_b200._lib import dptr, iptr
+        assert lib.tmg_inputs_rhs(g.nx, g.ny, iptr(fixed), len(fixed), iptr(ld), dptr(lv), len(lv), dptr(b)) == 1
+        assert np.all(b == 7.0)
+
+
+def test_host_length_checks_precede_device_work():
+    """Length / shape checks of the Python mirror raise the reference's
+    DimensionError before any device call (sparse.cpp:72-75, fem.cpp:286-289,
+    fem.cpp:295-298, mto.cpp:65-70)."""
+    import types
+
+    g = P.GridLevel(4, 4)
+    ops = types.SimpleNamespace(grid=g, lib=None, h=None)  # never reached
+    b = np.zeros(g.dof_count())
+    with pytest.raises(P.DimensionError, match="matvec: vector length 3 does not match matrix size 50"):
+        P.pcgmg_solve(ops, b, P.SolverConfig(), x0=np.zeros(3))
+    with pytest.raises(P.DimensionError, match="compliance: vector length 5"):
+        P.compliance(ops, np.zeros(5))
+    with pytest.raises(P.DimensionError, match="element_energies: vector length 5"):
+        P.element_energies(ops, np.zeros(5))
+    mat = P.MaterialModel()
+    with pytest.raises(P.DimensionError, match="sensitivities: density grid does not match level"):
+        P.sensitivities(ops, np.zeros((15, 4)), mat)
+    with pytest.raises(P.DimensionError, match="sensitivities: phase count mismatch"):
+        P.sensitivities(ops, np.zeros((16, 3)), mat)
+    with pytest.raises(P.DimensionError, match="element_energies: vector length 9"):
+        P.sensitivities(ops, np.zeros((16, 4)), mat, u=np.zeros(9))
+    with pytest.raises(P.DimensionError, match="filter: density grid does not match level"):
+        P.filter_sensitivities(ops, np.zeros(16), np.zeros((15, 4)), 0, 1.5)

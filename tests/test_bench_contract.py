@@ -32,3 +32,21 @@ def test_weak_scaling_mesh_grows_with_the_ranks():
 
 def test_reference_arm_uses_every_core():
     assert bench.host_cores() >= 1
+
+
+def test_gpus_flag_launches_one_rank_per_gpu():
+    """bench.py --gpus N outside torchrun starts N ranks itself (rank 0 prints
+    the line). On a GPU-less host both ranks get up to device init."""
+    import subprocess
+    import sys
+
+    import pytest
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("host has a GPU: the bench itself covers the launch")
+    p = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--config", "c0", "--steps", "1",
+                        "--warmup", "3", "--no-cpu-baseline"], capture_output=True, text=True, timeout=600)
+    err = p.stderr
+    assert "launching 2 ranks" in err
+    assert "rank 0/2" in err and "rank 1/2" in err

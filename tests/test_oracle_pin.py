@@ -243,3 +243,57 @@ def test_poisson_golden_bit_exact(tag, g):
     assert np.array_equal(r["solution"], d[tag + "_x"])
     assert np.array_equal(r["residual_history"], d[tag + "_hist"])
     assert np.array_equal(s.vcycle(d[tag + "_f"], np.zeros(s.n), 1, 2, 2), d[tag + "_vcycle"])
+
+
+def _make_golden():
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("make_golden", GOLDEN / "make_golden.py")
+    mg = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mg)
+    return mg
+
+
+@pytest.mark.parametrize("nx,ny,seed", [(8, 8, 0), (16, 12, 1), (24, 40, 7)])
+def test_bench_input_recipe_is_pinned(nx, ny, seed):
+    """The BASELINE density recipe (SURVEY.md 8(d): std::mt19937_64 with the
+    oracles.hpp:21-23 bit recipe) four ways, bit for bit: the product's host
+    generator (tmg_inputs_density_iid, which feeds every bench input), the
+    independent pure-Python restatement in make_golden.py, the C checker and
+    the reference's own oracle::Rng through oracle/_ref."""
+    import paper_2301_07457_b200 as P
+
+    mg = _make_golden()
+    want = mg.density(nx, ny, seed)
+    assert np.array_equal(P.density_iid(nx, ny, seed), want)
+    assert np.array_equal(po.density_iid("orc", nx, ny, seed), want)
+    if po.available("ref"):
+        assert np.array_equal(po.density_iid("ref", nx, ny, seed), want)
+        E = po.effective_moduli("ref", nx, ny, want, PHASES, 3.0)
+        assert np.array_equal(P.effective_moduli(want, P.MaterialModel()), E)
+
+
+def test_bench_input_recipe_at_scale():
+    """c1 (512^2, seed 0) and a 1024^2 seed-1 prefix of the c4 recipe: product,
+    C checker and reference generators agree bit for bit; the checkerboard
+    likewise (c2 recipe, 16x16 blocks)."""
+    import paper_2301_07457_b200 as P
+
+    kinds = ["orc"] + (["ref"] if po.available("ref") else [])
+    for nx, seed in ((512, 0), (1024, 1)):
+        a = P.density_iid(nx, nx, seed)
+        for k in kinds:
+            assert np.array_equal(po.density_iid(k, nx, nx, seed), a), (k, nx)
+    c = P.density_checker(256, 256, 16, 2)
+    for k in kinds:
+        assert np.array_equal(po.density_checker(k, 256, 256, 16, 2), c), k
+
+
+def test_bench_supports_and_load_match_the_product():
+    import paper_2301_07457_b200 as P
+
+    for nx, ny in ((8, 8), (16, 32)):
+        bc = P.wall_boundary_conditions(P.GridLevel(nx, ny), "uniform")
+        fixed, loads = po.wall_uniform_bc(nx, ny)
+        assert fixed == bc.fixed_dofs
+        assert loads == bc.point_loads
