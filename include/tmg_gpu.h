@@ -88,7 +88,9 @@ int tmg_gpu_create_local_slabs(int nx, int ny, int num_coarsenings, int dofs_per
  * all-reduce over NVLink / NVSwitch. nccl_unique_id: the 128-byte
  * ncclUniqueId created by rank 0 with tmg_nccl_unique_id and shared by the
  * caller. Host vectors passed to this handle are global; each rank reads and
- * writes only its own columns. */
+ * writes only its own columns. nranks = 1 is allowed: the slab machinery
+ * (all-reduced partials, halo calls, replicated coarse levels) then runs
+ * through a one-rank communicator and solves bitwise like tmg_gpu_create. */
 int tmg_gpu_create_nccl(int nx, int ny, int num_coarsenings, int dofs_per_node, int device, int nranks, int rank,
                         const void* nccl_unique_id, int replicated_level, tmg_gpu_handle** out);
 int tmg_nccl_unique_id(void* out128);

@@ -334,6 +334,10 @@ struct tmg_gpu_handle {
   cudaStream_t stream = nullptr;
   int nx = 0, ny = 0, nc = 0;
   int nranks = 1;  // global
+  // the slab machinery (partials all-reduced, ghost exchanges, replicated
+  // coarse levels) is on: several ranks, or an NCCL communicator of any size
+  // (a one-rank NCCL handle runs every exchange through NCCL)
+  bool distributed = false;
   int rep = 0;     // levels 0..rep are replicated on every rank
   std::vector<int> xpart;  // fine node-column partition, nranks + 1 entries
   std::vector<std::unique_ptr<Rank>> own;
@@ -357,6 +361,12 @@ struct tmg_gpu_handle {
   // scheme, conditional nodes on); the host launches it once per solve
   // (TMG_NO_DEVICE_LOOP=1 keeps the per-iteration host loop)
   bool device_loop = true;
+  // NCCL handles: conditional graph nodes (device-side stopping test and the
+  // one-graph loop) with the collectives inside their bodies. Every rank
+  // holds bitwise the same PCG scalars, so all take the same branches and
+  // issue the same collectives; opt-in (TMG_NCCL_COND_NODES=1) because only a
+  // one-rank communicator can be exercised on a one-GPU box
+  bool nccl_cond = false;
   // banded coarsest Cholesky (TMG_DENSE_COARSE_FACTOR=1: the dense kernel)
   bool band_factor = true;
   cudaGraphExec_t loop = nullptr;
@@ -387,8 +397,8 @@ struct tmg_gpu_handle {
   std::string err;
   int err_row = -1;
 
-  bool multi() const { return nranks > 1; }
-  bool dist(int l) const { return nranks > 1 && l > rep; }
+  bool multi() const { return distributed; }
+  bool dist(int l) const { return distributed && l > rep; }
   void count(long k = 1) {
     if (capturing) capture_kernels += k;
     else launches += k;
@@ -447,7 +457,6 @@ std::vector<int> partition(int nx, int ny, int nc, int rep, int nranks) {
 // highest replicated level: distribute level l while every rank owns >= 16
 // node columns of it
 int auto_rep(int nx, int nc, int nranks) {
-  if (nranks <= 1) return nc;
   int rep = nc;
   for (int l = nc; l >= 1; --l) {
     const int cols = (nx >> (nc - l)) + 1;
@@ -1280,7 +1289,7 @@ void capture_iteration(H* h, int gamma, int pre, int post) {
   // conditional nodes: not with NCCL collectives inside their bodies (that
   // transport cannot be exercised on a one-GPU box, so its graphs keep the
   // plain form)
-  const bool cond_ok = fused_upd && h->cond_nodes && (!h->comm || h->comm->local());
+  const bool cond_ok = fused_upd && h->cond_nodes && (!h->comm || h->comm->local() || h->nccl_cond);
   // graph slot g: 0/1 = iterations with (it-1)&1 == g (it >= 2 when fused),
   // 2 = iteration 1 of the fused scheme
   auto capture = [&](int g_slot) {
@@ -1699,8 +1708,9 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
   hp->nc = nc;
   hp->nranks = nranks;
   hp->red_tx = red_tx_of(nx, ny);
-  hp->rep = (nranks == 1) ? nc : (rep >= 0 ? std::min(rep, nc - 1) : auto_rep(nx, nc, nranks));
-  if (nranks > 1) {
+  hp->distributed = nranks > 1 || nccl_id != nullptr;
+  hp->rep = !hp->distributed ? nc : (rep >= 0 ? std::min(rep, nc - 1) : auto_rep(nx, nc, nranks));
+  if (hp->distributed) {
     if (nc < 1 || hp->rep >= nc) return cfg("a distributed solve needs at least the finest level distributed");
     hp->xpart = partition(nx, ny, nc, hp->rep, nranks);
     for (int r = 0; r < nranks; ++r)
@@ -1731,6 +1741,7 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
   if (const char* v = std::getenv("TMG_NO_COND_NODES")) hp->cond_nodes = std::atoi(v) == 0;
   if (const char* v = std::getenv("TMG_NO_DEVICE_LOOP")) hp->device_loop = std::atoi(v) == 0;
   if (const char* v = std::getenv("TMG_DENSE_COARSE_FACTOR")) hp->band_factor = std::atoi(v) == 0;
+  if (const char* v = std::getenv("TMG_NCCL_COND_NODES")) hp->nccl_cond = std::atoi(v) != 0;
   for (cudaEvent_t& e : hp->ev) CK(cudaEventCreate(&e));
   for (int i = 0; i < nlocal; ++i) {
     hp->own.push_back(std::make_unique<Rank>());
@@ -1739,7 +1750,7 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
     hp->ranks.push_back(&R);
     alloc_rank(hp, R);
   }
-  if (nranks > 1) {
+  if (hp->distributed) {
     if (nlocal > 1) hp->comm = std::make_unique<LocalComm>(hp->ranks);
     else hp->comm = std::make_unique<NcclComm>(nranks, rank, nccl_id);
   }
@@ -1805,7 +1816,7 @@ int tmg_nccl_unique_id(void* out128) {
 
 int tmg_partition(int nx, int ny, int num_coarsenings, int nranks, int replicated_level, int* x0s, int* rep_out) {
   if (nranks < 1 || num_coarsenings < 0 || nx < 1 || ny < 1) return TMG_ERR_CONFIG;
-  const int rep = nranks == 1 ? num_coarsenings
+  const int rep = nranks == 1 ? num_coarsenings  // (a single rank stores every level whole)
                               : (replicated_level >= 0 ? std::min(replicated_level, num_coarsenings - 1)
                                                        : auto_rep(nx, num_coarsenings, nranks));
   const std::vector<int> xp =

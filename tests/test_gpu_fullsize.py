@@ -13,6 +13,13 @@ reference's optimize()): compliance history to 1e-8 (warm-started tol-1e-8
 solves fix it only to about the solver tolerance: 7e-9 measured at outer
 iteration 4), PCG counts within +-2 and the design to the north-star 1e-6.
 
+c4 recipe at 4096^2 (the largest mesh the reference can assemble: its CSR
+offsets are int, sparse.hpp:53, and 8192^2 has ~2.42e9 nonzeros): against a
+fixture generated once from the unmodified reference (oracle/_ref) by
+tests/golden/make_c4_recipe_4096.py -- iteration count +-2, residual history,
+compliance 1e-9, u on a fixed dof sample 1e-8, |u| and four random
+projections of u.
+
 c4 (8192^2, 134M DOFs, 11 levels, the bench workload): size-independent
 properties only: the residual recomputed through a different kernel (the
 plain K.u pass) against the host right-hand side, compliance = b.u at
@@ -98,7 +105,11 @@ def test_c4_residual_compliance_determinism(c4):
     ops, b, nc = c4
     cfg = P.SolverConfig(tol=1e-8, max_iter=500, num_coarsenings=nc)
     rep = P.pcgmg_solve(ops, b, cfg)
-    assert rep.converged and rep.iterations == 21  # the bench workload's count (BASELINE recipe)
+    # the reference cannot run this mesh (int CSR offsets, sparse.hpp:53), so
+    # the count is not gated against it here; the c4 recipe is pinned against
+    # the reference at 4096^2 (test_c4_recipe_4096_matches_the_reference)
+    assert rep.converged
+    print(f"c4: {rep.iterations} PCG iterations")
     u = rep.solution
     # residual through the plain K.u pass (not the fused PCG kernels)
     r = b - ops.apply(nc, u)
@@ -141,3 +152,40 @@ def test_c3_first_outer_iterations():
     d = float(np.max(np.abs(got.density - want["density"])))
     print(f"c3 closed loop, {k} outer iterations: max |design diff| = {d:.2e}")
     assert d <= 1e-6
+
+
+def test_c4_recipe_4096_matches_the_reference():
+    """BASELINE c4's recipe (iid U(0,1) densities from seed 1, 10 levels down
+    to the 8x8 coarsest grid, tol 1e-8) at 4096^2 against the unmodified
+    reference's own pcgmg_solve (acceptance.cpp:156-190 drives it the same
+    way). The density generator is pinned bit for bit to the reference's
+    (tests/test_oracle_pin.py::test_bench_input_recipe_is_pinned)."""
+    import pathlib
+
+    fx = np.load(pathlib.Path(__file__).resolve().parent / "golden" / "c4_recipe_4096.npz")
+    n, nc, seed = int(fx["nx"]), int(fx["num_coarsenings"]), int(fx["seed"])
+    g = P.GridLevel(n, n)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    E = P.effective_moduli(P.density_iid(n, n, seed), MAT)
+    ops = P.MultigridOperators(g, nc, 0.3, bc)
+    ops.set_moduli(E, 0.6)
+    b = P.assemble_rhs(g, bc)
+    rep = P.pcgmg_solve(ops, b, P.SolverConfig(tol=1e-8, max_iter=5000, num_coarsenings=nc))
+    assert rep.converged and bool(fx["converged"])
+    ref_it = int(fx["iterations"])
+    print(f"4096^2 c4 recipe: device {rep.iterations} vs reference {ref_it} PCG iterations")
+    assert abs(rep.iterations - ref_it) <= 2
+    h = np.asarray(rep.residual_history)
+    hr = fx["residual_history"]
+    k = min(h.size, hr.size)
+    np.testing.assert_allclose(h[:k], hr[:k], rtol=1e-6)
+    u = rep.solution
+    idx = fx["sample_index"]
+    assert rel(u[idx], fx["u_sample"]) <= 1e-8
+    un = float(fx["u_norm"])
+    assert abs(np.linalg.norm(u) - un) <= 1e-9 * un
+    assert abs(P.compliance(ops) - float(fx["compliance"])) <= 1e-9 * abs(float(fx["compliance"]))
+    for s, p in zip(fx["proj_seeds"], fx["projections"]):
+        r = np.random.default_rng(int(s)).integers(0, 2, u.size, dtype=np.int8).astype(np.float64) * 2.0 - 1.0
+        # |r.(u - u_ref)| <= |r| |u - u_ref| = sqrt(n) |u - u_ref| <= sqrt(n) 1e-8 |u_ref|
+        assert abs(float(r @ u) - float(p)) <= 1e-8 * np.sqrt(u.size) * un

@@ -167,7 +167,10 @@ def test_tight_tolerance_matches_direct_solution(n, nc, recipe):
 def test_new_omega_on_a_live_handle_matches_a_fresh_handle():
     """omega is fixed when the operators are built (solvers.cpp:471): a setup
     with another omega on the same handle must solve exactly like a fresh
-    handle built with it (the captured graphs carry omega by value)."""
+    handle built with it (the captured graphs carry omega by value). With
+    omega = 0.9 the damped-Jacobi V-cycle is no longer positive definite on
+    this problem: the reference raises PreconditionerError at iteration 3, and
+    so must the live handle (stale omega-0.6 graphs would converge)."""
     nx = ny = 64
     nc = 3
     _, E = moduli(nx, ny)
@@ -175,18 +178,25 @@ def test_new_omega_on_a_live_handle_matches_a_fresh_handle():
     bc = P.wall_boundary_conditions(g, "uniform")
     b = P.assemble_rhs(g, bc)
     cfg = P.SolverConfig(tol=1e-8, max_iter=500)
+    checker = lambda om: po.System("orc", nx, ny, E, 0.3, bc.fixed_dofs, bc.point_loads).build_mg(nc, om)  # noqa
     live = P.MultigridOperators(g, nc, 0.3, bc)
     live.set_moduli(E, 0.6)
     first = P.pcgmg_solve(live, b, cfg)
     live.set_moduli(E, 0.9)
+    with pytest.raises(po.OracleError) as want_err:
+        checker(0.9).solve(b, tol=1e-8)
+    with pytest.raises(P.PreconditionerError) as got_err:
+        P.pcgmg_solve(live, b, cfg)
+    assert str(got_err.value) == want_err.value.msg
+    live.set_moduli(E, 0.7)
     again = P.pcgmg_solve(live, b, cfg)
     fresh = P.MultigridOperators(g, nc, 0.3, bc)
-    fresh.set_moduli(E, 0.9)
+    fresh.set_moduli(E, 0.7)
     want = P.pcgmg_solve(fresh, b, cfg)
     assert again.iterations == want.iterations
     assert np.array_equal(again.solution, want.solution)
     assert again.residual_history == want.residual_history
-    ref = po.System("orc", nx, ny, E, 0.3, bc.fixed_dofs, bc.point_loads).build_mg(nc, 0.9).solve(b, tol=1e-8)
+    ref = checker(0.7).solve(b, tol=1e-8)
     assert abs(again.iterations - ref["iterations"]) <= 2
     assert rel(again.solution, ref["solution"]) <= 1e-8
     assert first.residual_history != again.residual_history
