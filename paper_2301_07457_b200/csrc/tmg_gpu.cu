@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -52,6 +53,16 @@ struct TmgError {
 [[noreturn]] void fail(int code, const std::string& msg, int row = -1) {
   throw TmgError{code, msg, row};
 }
+
+// NVTX range for the phases the reference times with steady_clock
+// (solvers.cpp:335, 393; mto.cpp:264-350): setup, solve, outer iteration, OC
+// exchange. Header-only NVTX v3: free unless a profiler is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 #define CK(call)                                                                     \
   do {                                                                               \
@@ -1390,6 +1401,7 @@ void launch_cholesky(cudaStream_t s, double* A, int n, int* bad_row) {
 // ----------------------------------------------------------------- setup --
 
 void setup(H* h, double omega) {
+  NvtxRange nvtx("tmg.setup (Galerkin hierarchy + coarsest inverse)");
   if (!h->have_problem) fail(TMG_ERR_DIMENSION, "tmg_gpu_set_problem must precede setup");
   if (!h->have_moduli) fail(TMG_ERR_DIMENSION, "no element moduli uploaded");
   h->omega = omega;
@@ -1481,6 +1493,7 @@ struct SolveOut {
 };
 
 void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int pre, int post, SolveOut& o) {
+  NvtxRange nvtx("tmg.pcgmg_solve");
   need_setup(h);
   // SolverConfig::validate subset enforced by pcgmg_solve (solvers.cpp:518-521)
   if (pre != post) {
@@ -2137,6 +2150,7 @@ int oc_blocks() {
 // Throws TMG_ERR_MULTIPLIER (alpha unchanged) like the reference.
 void oc_pair_device(H* h, Rank& R, double* scratch, double* alpha, long ne, int np, double eps, int pa, int pb,
                     const double* sa, const double* sb, double target, const double* mv, double damping) {
+  NvtxRange nvtx("tmg.oc_update_pair");
   const int blocks = oc_blocks();
   OcArgs a{};
   a.ne = ne;
@@ -2311,6 +2325,7 @@ int tmg_gpu_optimize(tmg_gpu_handle* h, const tmg_optim_config* c, const double*
     bool have_u = false;
     const int reach = static_cast<int>(std::ceil(c->filter_radius)) - 1;
     for (int outer = 1; outer <= c->max_outer; ++outer) {
+      NvtxRange nvtx("tmg.optimize outer iteration");
       const auto t_iter = clk::now();
       // assemble_elasticity + build_multigrid_operators (mto.cpp:267-281)
       k_simp<<<dim3((g.ny + 127) / 128, g.nx), 128, 0, h->stream>>>(g, np, dens, pm, c->penalty, R.E);

@@ -15,7 +15,9 @@ acceptance.cpp:156-190 drives it, and stores what a full-size GPU test needs:
 the iteration count, the residual history, the compliance u^T K u, |u|_2, the
 sum of u, u on a fixed sample of dofs (every 1021st dof plus every top-edge
 v-dof) and u projected on four seeded random +-1 vectors (numpy PCG64, seeds
-11..14, regenerated at test time). Run once in this container (takes ~10 min
+11..14, regenerated at test time); then it continues the reference's solve
+from u to tol 1e-12 and stores that answer's compliance, sample and norm and
+|u - u_tight|, the reference's own distance to its converged solution. Run once in this container (takes ~10 min
 and ~41 GB of RAM); the fixture is committed, the test never needs
 /root/reference.
 """
@@ -69,13 +71,20 @@ def main():
     u = r["solution"]
     comp = s._f("system_compliance")(s.h, po._d(u))
     t = s.times()
+    # the reference's own distance to its converged answer (SURVEY.md 8(c)
+    # protocol, step 4): continue from u to tol 1e-12
+    rt = s.solve(b, tol=1e-12, max_iter=5000, gamma=1, pre=2, post=2, x0=u)
+    ut = rt["solution"]
+    comp_t = s._f("system_compliance")(s.h, po._d(ut))
     idx = sample_index(N, N)
     np.savez_compressed(
         pathlib.Path(__file__).resolve().parent / "c4_recipe_4096.npz",
         nx=N, ny=N, num_coarsenings=NC, seed=SEED, iterations=r["iterations"], converged=r["converged"],
         residual_history=r["residual_history"], compliance=comp, u_norm=np.linalg.norm(u), u_sum=u.sum(),
         sample_index=idx, u_sample=u[idx], projections=projections(u), proj_seeds=np.array(PROJ_SEEDS),
-        ref_seconds=np.array([t["assemble"], t["setup"], t["pcg"]]))
+        ref_seconds=np.array([t["assemble"], t["setup"], t["pcg"]]),
+        tight_iterations=rt["iterations"], compliance_tight=comp_t, u_sample_tight=ut[idx],
+        u_norm_tight=np.linalg.norm(ut), u_dist_tight=np.linalg.norm(u - ut))
     print(f"iterations {r['iterations']} converged {r['converged']} compliance {comp!r} "
           f"assemble {t['assemble']:.1f} s setup {t['setup']:.1f} s pcg {t['pcg']:.1f} s "
           f"total {time.time() - t0:.1f} s", flush=True)

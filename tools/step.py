@@ -20,10 +20,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4", choices=sorted(bench.CONFIGS))
 ap.add_argument("--solves", type=int, default=1)
 ap.add_argument("--kernels", type=int, default=0, help="also time K.u / sweep this many reps")
+ap.add_argument("--slabs", type=int, default=1, help="x-slabs driven from this process (LocalComm)")
+ap.add_argument("--rep", type=int, default=-1, help="replicated level of the slab decomposition")
 a = ap.parse_args()
 nx, ny, nc, recipe, seed, desc = bench.CONFIGS[a.config]
 g, bc, E, b = bench.make_inputs(nx, ny, recipe, seed)
-ops = P.MultigridOperators(g, nc, 0.3, bc)
+ops = P.MultigridOperators(g, nc, 0.3, bc, slabs=a.slabs, replicated_level=a.rep)
 ops.set_moduli(E, bench.OMEGA)
 lib = P._lib.load()
 ops._check(lib.tmg_gpu_upload_rhs(ops.h, P._lib.dptr(b)))
@@ -33,7 +35,8 @@ for _ in range(a.solves):
     ops._check(lib.tmg_gpu_setup(ops.h, bench.OMEGA))
     ops._check(lib.tmg_gpu_solve_resident(ops.h, 0, 1e-8, 5000, 1, 2, 2, C.byref(it), C.byref(fr), C.byref(cv),
                                           C.byref(sec), P._lib.dptr(hist), hist.size, C.byref(hl)))
-    print(f"{desc}: iterations={it.value} relres={fr.value:.3e} pcg={sec.value * 1e3:.2f} ms", flush=True)
+    print(f"{desc} [{a.slabs} slab(s)]: iterations={it.value} relres={fr.value:.3e} pcg={sec.value * 1e3:.2f} ms "
+          f"({sec.value * 1e3 / max(it.value, 1):.3f} ms/iteration)", flush=True)
 if a.kernels:
     for w, name in ((0, "K.u"), (1, "sweep")):
         ms, by = ops.time_kernel(w, a.kernels)
