@@ -354,6 +354,11 @@ struct tmg_gpu_handle {
   std::vector<std::unique_ptr<Rank>> own;
   std::vector<Rank*> ranks;  // ranks driven by this process
   std::unique_ptr<Comm> comm;
+  // several ranks in this process: one stream per rank, forked from and
+  // joined back into `stream` around every pass (for_ranks)
+  std::vector<cudaStream_t> rstreams;
+  cudaEvent_t fork_ev = nullptr;
+  std::vector<cudaEvent_t> join_ev;
   double nu = 0.3;
   double ke[64];
   bool have_problem = false, have_moduli = false, have_setup = false, have_solution = false;
@@ -566,6 +571,9 @@ void free_handle(H* h) {
   if (h->loop) cudaGraphExecDestroy(h->loop);
   h->comm.reset();
   for (Rank* R : h->ranks) free_rank(*R);
+  for (cudaStream_t s : h->rstreams) cudaStreamDestroy(s);
+  for (cudaEvent_t e : h->join_ev) cudaEventDestroy(e);
+  if (h->fork_ev) cudaEventDestroy(h->fork_ev);
   for (cudaEvent_t e : h->ev)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : h->uev)
@@ -670,6 +678,35 @@ void gather_level(H* h, int l, const std::function<void*(Rank&)>& field, size_t 
   h->comm->gather_columns(h->ranks, l, field, esize, plane_stride, planes, X0, n, h->stream);
 }
 
+// Per-rank work of one pass. With several ranks in this process (LocalComm)
+// each rank's launches go on its own stream between a fork from and a join
+// into the handle's stream, so the slabs run concurrently on the device as
+// they would on N GPUs and the captured graphs hold N parallel branches; the
+// exchanges (halos, all-reduce, gathers) stay on the handle's stream between
+// the joins. One rank: a plain call.
+template <class F>
+void for_ranks(H* h, F&& fn) {
+  if (h->rstreams.empty()) {
+    for (Rank* R : h->ranks) fn(*R);
+    return;
+  }
+  cudaStream_t main = h->stream;
+  CK(cudaEventRecord(h->fork_ev, main));
+  for (size_t i = 0; i < h->ranks.size(); ++i) {
+    CK(cudaStreamWaitEvent(h->rstreams[i], h->fork_ev, 0));
+    h->stream = h->rstreams[i];
+    try {
+      fn(*h->ranks[i]);
+    } catch (...) {
+      h->stream = main;
+      throw;
+    }
+    h->stream = main;
+    CK(cudaEventRecord(h->join_ev[i], h->rstreams[i]));
+  }
+  for (cudaEvent_t e : h->join_ev) CK(cudaStreamWaitEvent(main, e, 0));
+}
+
 // ---------------------------------------------------------- reductions ----
 
 // Launch a reduction on every rank: single rank -> the kernel's last block
@@ -683,7 +720,7 @@ void reduce(H* h, RedOp op, const std::function<void(Rank&, RedOp, double*)>& la
     launch(R, op, want_out ? R.scal : nullptr);
     return;
   }
-  for (Rank* R : h->ranks) launch(*R, op, nullptr);
+  for_ranks(h, [&](Rank& R) { launch(R, op, nullptr); });
   const int n = red_tiles(h, h->ranks[0]->fine().g).nparts;
   h->comm->allreduce(h->ranks, n, h->stream);
   for (Rank* R : h->ranks) {
@@ -968,7 +1005,7 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
                    int upd_k = -1, const std::function<void()>& after_update = nullptr) {
   auto& rs = h->ranks;
   if (l == 0) {
-    for (Rank* R : rs) coarse_solve(h, *R, R->lev[0].f, R->lev[0].u[R->lev[0].cur]);
+    for_ranks(h, [&](Rank& R) { coarse_solve(h, R, R.lev[0].f, R.lev[0].u[R.lev[0].cur]); });
     return false;
   }
   const bool fine = (l == h->nc);
@@ -1003,12 +1040,13 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
     if (after_update) after_update();
   } else if (fine && zero && pre >= 2) {
     // the finest f (the PCG residual) already carries its halo
-    for (Rank* R : rs) {
+    for_ranks(h, [&](Rank& Rk) {
+      Rank* R = &Rk;
       MarchArgs a = march_args(h, *R, nullptr);
       a.f = R->lev[l].f;
       a.out0 = nxt(*R);
       launch_march<StSweep01, false>(h, a);
-    }
+    });
     flip();
     s = 2;
     zero = false;
@@ -1021,7 +1059,7 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
     // coarse level: both pre-sweeps, the residual and the restriction in one
     // pass over the stencil (tmg_smarch.cuh)
     halo_vec(h, l, [&](Rank& R) { return R.lev[l].f; }, 3, 2);
-    for (Rank* R : rs) launch_smarch<false>(h, *R, l, nullptr, nullptr, nxt(*R), R->lev[l - 1].f);
+    for_ranks(h, [&](Rank& R) { launch_smarch<false>(h, R, l, nullptr, nullptr, nxt(R), R.lev[l - 1].f); });
     flip();
     s = 2;
     zero = false;
@@ -1029,29 +1067,30 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
   }
   for (; s < pre; ++s) {
     if (!zero) halo_vec(h, l, cur);
-    for (Rank* R : rs) sweep_level(h, *R, l, zero, cur(*R), nxt(*R), R->lev[l].f);
+    for_ranks(h, [&](Rank& R) { sweep_level(h, R, l, zero, cur(R), nxt(R), R.lev[l].f); });
     flip();
     zero = false;
   }
   if (restricted) {
   } else if (zero) {
     halo_vec(h, l, [&](Rank& R) { return R.lev[l].f; });
-    for (Rank* R : rs) restrict_level(h, *R, l, R->lev[l].f, R->lev[l - 1].f);
+    for_ranks(h, [&](Rank& R) { restrict_level(h, R, l, R.lev[l].f, R.lev[l - 1].f); });
   } else if (fine) {
     halo_vec(h, l, cur, 2, 1);
-    for (Rank* R : rs) {
+    for_ranks(h, [&](Rank& Rk) {
+      Rank* R = &Rk;
       MarchArgs a = march_args(h, *R, cur(*R));
       long coff;
       a.gc = coarse_of(h, *R, l, coff);
       a.f = R->lev[l].f;
       a.out0 = R->lev[l - 1].f + coff;
       launch_march<StResidRestrict, false>(h, a);
-    }
+    });
   } else {
     halo_vec(h, l, cur);
-    for (Rank* R : rs) residual_level(h, *R, l, cur(*R), R->lev[l].f, R->lev[l].res);
+    for_ranks(h, [&](Rank& R) { residual_level(h, R, l, cur(R), R.lev[l].f, R.lev[l].res); });
     halo_vec(h, l, [&](Rank& R) { return R.lev[l].res; });
-    for (Rank* R : rs) restrict_level(h, *R, l, R->lev[l].res, R->lev[l - 1].f);
+    for_ranks(h, [&](Rank& R) { restrict_level(h, R, l, R.lev[l].res, R.lev[l - 1].f); });
   }
   if (dist && !cdist) gather_level(h, l - 1, [&](Rank& R) -> void* { return R.lev[l - 1].f; }, sizeof(double2), 0, 1);
   const int visits = fine ? 1 : gamma;
@@ -1065,11 +1104,12 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
     // coarse level: prolongation + both post-sweeps in one pass
     halo_vec(h, l, cur, 2, 2);
     halo_vec(h, l, [&](Rank& R) { return R.lev[l].f; }, 3, 2);
-    for (Rank* R : rs) launch_smarch<true>(h, *R, l, cur(*R), ccur(*R), nxt(*R), nullptr);
+    for_ranks(h, [&](Rank& R) { launch_smarch<true>(h, R, l, cur(R), ccur(R), nxt(R), nullptr); });
     flip();
     p = post;
   } else if (fine && !zero && post >= 1) {
-    for (Rank* R : rs) {
+    for_ranks(h, [&](Rank& Rk) {
+      Rank* R = &Rk;
       MarchArgs a = march_args(h, *R, cur(*R));
       long coff;
       a.gc = coarse_of(h, *R, l, coff);
@@ -1077,11 +1117,11 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
       a.f = R->lev[l].f;
       a.out0 = nxt(*R);
       launch_march<StProlongSweep, false>(h, a);
-    }
+    });
     flip();
     p = 1;
   } else {
-    for (Rank* R : rs) prolong_level(h, *R, l, ccur(*R), cur(*R), !zero);
+    for_ranks(h, [&](Rank& R) { prolong_level(h, R, l, ccur(R), cur(R), !zero); });
   }
   bool fused = false;
   for (; p < post; ++p) {
@@ -1098,7 +1138,7 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
       });
       fused = true;
     } else {
-      for (Rank* R : rs) sweep_level(h, *R, l, false, cur(*R), nxt(*R), R->lev[l].f);
+      for_ranks(h, [&](Rank& R) { sweep_level(h, R, l, false, cur(R), nxt(R), R.lev[l].f); });
     }
     flip();
   }
@@ -1389,7 +1429,7 @@ int coarsest_band(const Grid& g0, int n) { return std::min(n - 1, 2 * (g0.ny + 2
 // dense Cholesky of the coarsest matrix, in shared memory when it fits
 void launch_cholesky(cudaStream_t s, double* A, int n, int* bad_row) {
   if (n <= kCholSmemMax) {
-    const size_t sm = sizeof(double) * n * n;
+    const size_t sm = sizeof(double) * (n * n + n);
     CK(cudaFuncSetAttribute(k_cholesky<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
     k_cholesky<true><<<1, 1024, sm, s>>>(A, n, bad_row);
   } else {
@@ -1408,7 +1448,8 @@ void setup(H* h, double omega) {
   h->have_setup = false;
   // Galerkin hierarchy, finest to coarsest (solvers.cpp:474-478)
   for (int l = h->nc; l >= 1; --l) {
-    for (Rank* R : h->ranks) {
+    for_ranks(h, [&](Rank& Rk) {
+      Rank* R = &Rk;
       long off;
       const Grid cg = coarse_of(h, *R, l, off);
       dim3 blk(32, 4), grd((cg.ny + 1 + 31) / 32, (cg.ncol + 3) / 4);
@@ -1425,7 +1466,7 @@ void setup(H* h, double omega) {
       }
       CKL();
       h->count();
-    }
+    });
     if (h->dist(l - 1)) {
       // ghost columns of the new level's stencil (backward blocks, Galerkin
       // of the next level reads two columns to the left)
@@ -1448,7 +1489,7 @@ void setup(H* h, double omega) {
     });
     CKL();
     const int b = coarsest_band(g0, n);
-    const size_t bsm = static_cast<size_t>(n) * (b + 1) * sizeof(double);
+    const size_t bsm = static_cast<size_t>(n) * (b + 2) * sizeof(double);
     if (h->band_factor && b <= 31 && bsm <= 200 * 1024) {
       CK(cudaFuncSetAttribute(k_cholesky_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bsm)));
       k_cholesky_band<<<1, 32, bsm, h->stream>>>(R->A0, n, b, R->bad_row);
@@ -1764,7 +1805,18 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
     alloc_rank(hp, R);
   }
   if (hp->distributed) {
-    if (nlocal > 1) hp->comm = std::make_unique<LocalComm>(hp->ranks);
+    if (nlocal > 1) {
+      hp->comm = std::make_unique<LocalComm>(hp->ranks);
+      CK(cudaEventCreateWithFlags(&hp->fork_ev, cudaEventDisableTiming));
+      for (int i = 0; i < nlocal; ++i) {
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        hp->rstreams.push_back(s);
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        hp->join_ev.push_back(e);
+      }
+    }
     else hp->comm = std::make_unique<NcclComm>(nranks, rank, nccl_id);
   }
   CK(cudaStreamSynchronize(hp->stream));
@@ -1883,7 +1935,7 @@ int tmg_gpu_set_problem(tmg_gpu_handle* h, double nu, const int* fixed_dofs, int
     CK(cudaMemcpyToSymbolAsync(c_k8, h->ke, 8 * sizeof(double), 0, cudaMemcpyHostToDevice, h->stream));  // row 0
     CK(cudaMemcpyToSymbolAsync(c_ke64, h->ke, 64 * sizeof(double), 0, cudaMemcpyHostToDevice, h->stream));
     // M_q = (1/4) P_q^T Ke P_q of the four element quadrants of a coarse cell
-    // (k_galerkin_cells), from the Ke the device applies (8 values, ke_perm)
+    // (k_galerkin_cells), from the exact Ke the device applies
     {
       double mq[4][64];
       auto w1 = [](int f, int cc) { return f == 2 * cc ? 1.0L : (f == 1 ? 0.5L : 0.0L); };
@@ -1900,7 +1952,7 @@ int tmg_gpu_set_problem(tmg_gpu_handle* h, double nu, const int* fixed_dofs, int
           for (int b = 0; b < 8; ++b) {
             long double acc = 0.0L;
             for (int r = 0; r < 8; ++r)
-              for (int c = 0; c < 8; ++c) acc += Pm[r][a] * static_cast<long double>(h->ke[ke_perm(r, c)]) * Pm[c][b];
+              for (int c = 0; c < 8; ++c) acc += Pm[r][a] * static_cast<long double>(h->ke[r * 8 + c]) * Pm[c][b];
             mq[q][a * 8 + b] = static_cast<double>(0.25L * acc);
           }
       }

@@ -502,9 +502,23 @@ __global__ void k_dense_assemble(Op op, Grid g, double* __restrict__ A, int n) {
     }
 }
 
+// Singular pivot test of the coarsest factorizations. CholeskyFactor::factor
+// (solvers.cpp:144-148) raises DefinitenessError at the first pivot that is
+// not > 0. For a matrix that is singular in exact arithmetic (an
+// unconstrained structure: three rigid motions) that pivot is a rounding
+// residue of either sign, and the device's Galerkin operator is not bitwise
+// the reference's, so the device also treats a pivot within 16 n eps of the
+// row's original diagonal as zero: it then stops at the same (first
+// dependent) row as the reference. Legitimate coarsest pivots sit far above
+// it (a stiff island held only by 1e-9 void still has ~1e-9 relative pivots,
+// 16 n eps = 6e-13 at n = 162).
+__device__ __forceinline__ bool pivot_ok(double d, double diag0, int n) {
+  return d > 0.0 && d > 16.0 * n * 2.220446049250313e-16 * fabs(diag0);
+}
+
 // Right-looking Cholesky, lower triangle in place, one CTA (n <= 2048).
-// A non-positive pivot records its row like CholeskyFactor::factor
-// (solvers.cpp:144-148).
+// A non-positive (or numerically zero, pivot_ok) pivot records its row like
+// CholeskyFactor::factor (solvers.cpp:144-148).
 // SMEM: the matrix is factored in shared memory (n <= kCholSmemMax; the
 // same operations in the same order, so the factor is bit-identical).
 constexpr int kCholSmemMax = 168;  // 168^2 doubles = 220.5 KB
@@ -520,12 +534,14 @@ __global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ Ag, int 
     // scaled column is also staged contiguously (cv) so the trailing update
     // reads it without the bank conflicts of the strided column
     __shared__ double cv[kCholSmemMax];
+    double* dg0 = As + n * n;  // original diagonal
     for (int k = t; k < n * n; k += nt) As[k] = Ag[k];
+    for (int k = t; k < n; k += nt) dg0[k] = Ag[static_cast<long>(k) * n + k];
     __syncthreads();
     int bad = -1;
     for (int k = 0; k < n; ++k) {
       const double d = A[k * n + k];
-      if (!(d > 0.0)) {  // the same d in every thread: a uniform exit
+      if (!pivot_ok(d, dg0[k], n)) {  // the same d in every thread: a uniform exit
         bad = k;
         break;
       }
@@ -553,12 +569,14 @@ __global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ Ag, int 
     if (t == 0) *bad_row = bad;
     return;
   }
+  __shared__ double dg0g[SMEM ? 1 : 2048];
   if (t == 0) fail = -1;
+  for (int k = t; k < n; k += nt) dg0g[k] = Ag[static_cast<long>(k) * n + k];
   __syncthreads();
   for (int k = 0; k < n; ++k) {
     if (t == 0) {
       const double d = A[static_cast<long>(k) * n + k];
-      if (!(d > 0.0)) fail = k;
+      if (!pivot_ok(d, dg0g[k], n)) fail = k;
       else A[static_cast<long>(k) * n + k] = sqrt(d);
     }
     __syncthreads();
@@ -592,15 +610,17 @@ __global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ Ag, int 
 __global__ void __launch_bounds__(32) k_cholesky_band(double* __restrict__ Ag, int n, int b, int* bad_row) {
   extern __shared__ double Bs[];
   const int lane = threadIdx.x, W = b + 1;
+  double* dg0 = Bs + n * W;  // original diagonal
   for (int e = lane; e < n * W; e += 32) {
     const int i = e / W, d = e - i * W;
     Bs[e] = (i - d >= 0) ? Ag[static_cast<long>(i) * n + i - d] : 0.0;
   }
+  for (int k = lane; k < n; k += 32) dg0[k] = Ag[static_cast<long>(k) * n + k];
   __syncwarp();
   int bad = -1;
   for (int k = 0; k < n; ++k) {
     const double dk = Bs[k * W];
-    if (!(dk > 0.0)) {  // the same value in every lane: a uniform exit
+    if (!pivot_ok(dk, dg0[k], n)) {  // the same value in every lane: a uniform exit
       bad = k;
       break;
     }

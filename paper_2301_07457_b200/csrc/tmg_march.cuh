@@ -145,26 +145,29 @@ __device__ __forceinline__ double2 masked2(double2 v, uint32_t byte) {
   return v;
 }
 
-// rows (2A, 2A+1) of e * Ke times the element's corner values q0..q3
-template <int A>
+// rows (2A, 2A+1) of e * Ke times the element's corner values q0..q3; EX:
+// the exact quadrature Ke (the system's operator), else the 8-value form
+// (the V-cycle's smoothing passes; tmg_device.cuh)
+#define TMG_KE(r, b) (EX ? c_kex_at((r), (b)) : c_ke_at((r), (b)))
+template <int A, bool EX>
 __device__ __forceinline__ void erows(double e, const double2& q0, const double2& q1, const double2& q2,
                                       const double2& q3, double& y0, double& y1) {
-  double s0 = c_ke_at(2 * A, 0) * q0.x;
-  s0 = fma(c_ke_at(2 * A, 1), q0.y, s0);
-  s0 = fma(c_ke_at(2 * A, 2), q1.x, s0);
-  s0 = fma(c_ke_at(2 * A, 3), q1.y, s0);
-  s0 = fma(c_ke_at(2 * A, 4), q2.x, s0);
-  s0 = fma(c_ke_at(2 * A, 5), q2.y, s0);
-  s0 = fma(c_ke_at(2 * A, 6), q3.x, s0);
-  s0 = fma(c_ke_at(2 * A, 7), q3.y, s0);
-  double s1 = c_ke_at(2 * A + 1, 0) * q0.x;
-  s1 = fma(c_ke_at(2 * A + 1, 1), q0.y, s1);
-  s1 = fma(c_ke_at(2 * A + 1, 2), q1.x, s1);
-  s1 = fma(c_ke_at(2 * A + 1, 3), q1.y, s1);
-  s1 = fma(c_ke_at(2 * A + 1, 4), q2.x, s1);
-  s1 = fma(c_ke_at(2 * A + 1, 5), q2.y, s1);
-  s1 = fma(c_ke_at(2 * A + 1, 6), q3.x, s1);
-  s1 = fma(c_ke_at(2 * A + 1, 7), q3.y, s1);
+  double s0 = TMG_KE(2 * A, 0) * q0.x;
+  s0 = fma(TMG_KE(2 * A, 1), q0.y, s0);
+  s0 = fma(TMG_KE(2 * A, 2), q1.x, s0);
+  s0 = fma(TMG_KE(2 * A, 3), q1.y, s0);
+  s0 = fma(TMG_KE(2 * A, 4), q2.x, s0);
+  s0 = fma(TMG_KE(2 * A, 5), q2.y, s0);
+  s0 = fma(TMG_KE(2 * A, 6), q3.x, s0);
+  s0 = fma(TMG_KE(2 * A, 7), q3.y, s0);
+  double s1 = TMG_KE(2 * A + 1, 0) * q0.x;
+  s1 = fma(TMG_KE(2 * A + 1, 1), q0.y, s1);
+  s1 = fma(TMG_KE(2 * A + 1, 2), q1.x, s1);
+  s1 = fma(TMG_KE(2 * A + 1, 3), q1.y, s1);
+  s1 = fma(TMG_KE(2 * A + 1, 4), q2.x, s1);
+  s1 = fma(TMG_KE(2 * A + 1, 5), q2.y, s1);
+  s1 = fma(TMG_KE(2 * A + 1, 6), q3.x, s1);
+  s1 = fma(TMG_KE(2 * A + 1, 7), q3.y, s1);
   y0 = fma(e, s0, y0);
   y1 = fma(e, s1, y1);
 }
@@ -172,25 +175,27 @@ __device__ __forceinline__ void erows(double e, const double2& q0, const double2
 // K w at the centre of the 3x3 window (l/c/r = columns x-1/x/x+1, index
 // 0/1/2 = rows y-1/y/y+1). Elements (x-1,y-1) eA, (x,y-1) eB, (x,y) eC,
 // (x-1,y) eD hold the node at their corners 2, 3, 0, 1 (fem.cpp:83-86).
+template <bool EX>
 __device__ __forceinline__ void gather9(const double2 (&l)[3], const double2 (&c)[3], const double2 (&r)[3],
                                         double eA, double eB, double eC, double eD, double& y0,
                                         double& y1) {
   y0 = 0.0;
   y1 = 0.0;
-  erows<2>(eA, l[0], c[0], c[1], l[1], y0, y1);
-  erows<3>(eB, c[0], r[0], r[1], c[1], y0, y1);
-  erows<0>(eC, c[1], r[1], r[2], c[2], y0, y1);
-  erows<1>(eD, l[1], c[1], c[2], l[2], y0, y1);
+  erows<2, EX>(eA, l[0], c[0], c[1], l[1], y0, y1);
+  erows<3, EX>(eB, c[0], r[0], r[1], c[1], y0, y1);
+  erows<0, EX>(eC, c[1], r[1], r[2], c[2], y0, y1);
+  erows<1, EX>(eD, l[1], c[1], c[2], l[2], y0, y1);
 }
 
 // (A w)_i and diag(A)_i of Z K Z + I_fixed (fem.cpp:89-106) for the window.
 // mL/mC/mR: the three mask bytes (rows y-1, y, y+1) of each column.
+template <bool EX = false>
 __device__ __forceinline__ void fine_apply(const double2 (&l)[3], const double2 (&c)[3], const double2 (&r)[3],
                                            uint32_t mL, uint32_t mC, uint32_t mR, double eA, double eB,
                                            double eC, double eD, double2& y, double2& d) {
   double y0, y1;
   if ((mL | mC | mR) == 0u) {
-    gather9(l, c, r, eA, eB, eC, eD, y0, y1);
+    gather9<EX>(l, c, r, eA, eB, eC, eD, y0, y1);
   } else {
     double2 ml[3], mc[3], mr[3];
 #pragma unroll
@@ -199,10 +204,10 @@ __device__ __forceinline__ void fine_apply(const double2 (&l)[3], const double2 
       mc[q] = masked2(c[q], (mC >> (8 * q)) & 0xFFu);
       mr[q] = masked2(r[q], (mR >> (8 * q)) & 0xFFu);
     }
-    gather9(ml, mc, mr, eA, eB, eC, eD, y0, y1);
+    gather9<EX>(ml, mc, mr, eA, eB, eC, eD, y0, y1);
   }
-  double d0 = c_k8[0] * ((eA + eB) + (eC + eD));  // every Ke diagonal entry is k0
-  double d1 = d0;
+  const double2 kd = ke_diag(eA, eB, eC, eD);  // the reference's diagonal, bitwise
+  double d0 = kd.x, d1 = kd.y;
   const uint32_t own = (mC >> 8) & 0xFFu;
   if (own) {
     const int k0 = own & 15, k1 = (own >> 4) & 15;
@@ -221,8 +226,8 @@ __device__ __forceinline__ void fine_apply(const double2 (&l)[3], const double2 
 
 // diagonal of a node from its four element moduli and own mask byte
 __device__ __forceinline__ double2 fine_diag(double eA, double eB, double eC, double eD, uint32_t own) {
-  double d0 = c_k8[0] * ((eA + eB) + (eC + eD));
-  double d1 = d0;
+  const double2 kd = ke_diag(eA, eB, eC, eD);
+  double d0 = kd.x, d1 = kd.y;
   if (own) {
     const int k0 = own & 15, k1 = (own >> 4) & 15;
     if (k0) d0 = k0;
@@ -291,8 +296,9 @@ __device__ __forceinline__ void load_window(const unsigned char* s, int ou, int 
   c.m3 = mask3(s, om, mis[2], t);
 }
 
+template <bool EX = false>
 __device__ __forceinline__ void window_apply(const Col& L, const Col& C, const Col& R, double2& y, double2& d) {
-  fine_apply(L.u, C.u, R.u, L.m3, C.m3, R.m3, L.e1, C.e1, C.e2, L.e2, y, d);
+  fine_apply<EX>(L.u, C.u, R.u, L.m3, C.m3, R.m3, L.e1, C.e1, C.e2, L.e2, y, d);
 }
 
 // y = A u (K1); optional partial u.Au
@@ -314,7 +320,7 @@ struct StApply {
                              const int*, int x, int yt, int, bool live, double& part, double2&) {
     if (!live) return;
     double2 y, d;
-    window_apply(L, C, R, y, d);
+    window_apply<true>(L, C, R, y, d);
     a.out0[a.g.idx(x, yt)] = y;
     if (DOT) part = fma(C.u[1].x, y.x, fma(C.u[1].y, y.y, part));
   }
@@ -603,7 +609,7 @@ struct StPupd {
                              const int*, int x, int yt, int, bool live, double& part, double2&) {
     if (!live) return;
     double2 y, d;
-    window_apply(L, C, R, y, d);
+    window_apply<true>(L, C, R, y, d);
     const long i = a.g.idx(x, yt);
     a.out0[i] = C.u[1];
     a.out1[i] = y;

@@ -285,9 +285,15 @@ def test_errors_mirror_reference():
     with pytest.raises(P.ConfigError):
         P.MultigridOperators(P.GridLevel(8, 8), 1, 0.3, P.BoundaryConditions([1000], []))
     # unconstrained structure: singular coarsest operator (solvers.cpp:144-148)
+    # the reference stops at row 14, the first dependent row (its pivot there
+    # is a rounding residue); the device treats a pivot within 16 n eps of
+    # the row's diagonal as zero and stops at the same row
     free = P.MultigridOperators(P.GridLevel(8, 8), 2, 0.3, P.BoundaryConditions([], []))
-    with pytest.raises(P.DefinitenessError):
+    with pytest.raises(P.DefinitenessError) as err:
         free.set_moduli(np.ones(64))
+    with pytest.raises(po.OracleError) as want:
+        po.System("orc", 8, 8, np.ones(64), 0.3, [], []).build_mg(2)
+    assert err.value.row == want.value.row == 14
 
 
 def test_duplicate_fixed_dofs_follow_finish_assembly():
