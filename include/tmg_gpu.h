@@ -59,7 +59,10 @@ typedef struct tmg_gpu_handle tmg_gpu_handle;
 /* Replaces build_hierarchy(nx, ny, num_coarsenings, 2) (grid.cpp:53-96) and
  * the device allocation for all levels. Same ConfigError cases: nx, ny >= 1,
  * num_coarsenings >= 0, divisibility by 2^num_coarsenings. dofs_per_node must
- * be 2 (plane elasticity). device = CUDA ordinal. */
+ * be 2 (plane elasticity). device = CUDA ordinal. Limit (no reference twin):
+ * the coarsest level, solved through a dense explicit inverse, may have at
+ * most 2048 dofs, i.e. 2 (nx/2^nc + 1)(ny/2^nc + 1) <= 2048 (ConfigError
+ * otherwise; every BASELINE configuration coarsens to 8x8 = 162 dofs). */
 int tmg_gpu_create(int nx, int ny, int num_coarsenings, int dofs_per_node,
                    int device, tmg_gpu_handle** out);
 void tmg_gpu_destroy(tmg_gpu_handle* h);

@@ -296,7 +296,10 @@ __device__ __forceinline__ void load_window(const unsigned char* s, int ou, int 
   c.m3 = mask3(s, om, mis[2], t);
 }
 
-template <bool EX = false>
+#ifndef TMG_EXACT_SMOOTHER
+#define TMG_EXACT_SMOOTHER 0
+#endif
+template <bool EX = TMG_EXACT_SMOOTHER>
 __device__ __forceinline__ void window_apply(const Col& L, const Col& C, const Col& R, double2& y, double2& d) {
   fine_apply<EX>(L.u, C.u, R.u, L.m3, C.m3, R.m3, L.e1, C.e1, C.e2, L.e2, y, d);
 }
