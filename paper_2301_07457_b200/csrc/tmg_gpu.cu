@@ -436,8 +436,17 @@ using H = tmg_gpu_handle;
 // each of 148 SMs (ties to the wider strip). On c1-c4 it is the width the
 // passes used before (8-64); meshes of ~64^2 get 1-column strips, whose
 // passes are 4 column steps long instead of 11.
+// nominal resident CTAs per SM of the strip-width model (TMG_STRIP_SLOTS
+// overrides it; read once per process, so every handle tiles alike)
+long strip_slots_per_sm() {
+  static const long v = [] {
+    const char* e = std::getenv("TMG_STRIP_SLOTS");
+    return e ? std::max(1L, std::atol(e)) : 3L;
+  }();
+  return v;
+}
 int pow2_strip(long rows_tiles, long cols, int a) {
-  const long slots = 3L * 148;
+  const long slots = strip_slots_per_sm() * 148;
   int best = 64;
   long best_cost = -1;
   for (int tx = 64; tx >= 1; tx /= 2) {

@@ -114,9 +114,11 @@ __device__ __forceinline__ double oc_cand(const double4 v, const OcStep& s) {
   const double p = s.half ? v.w * s.scale : exp(s.damping * (v.w - s.scale));
   return s_clamp(v.x * p, v.y, v.z);
 }
+// plain L2-coherent loads (ld.global.cg), not the read-only path: the kernel
+// itself rewrites the gain word of every record before the bisection steps
 __device__ __forceinline__ double4 ld_el(const double4* p) {
   const double2* q = reinterpret_cast<const double2*>(p);
-  const double2 u = __ldg(q), w = __ldg(q + 1);
+  const double2 u = __ldcg(q), w = __ldcg(q + 1);
   return make_double4(u.x, u.y, w.x, w.y);
 }
 
