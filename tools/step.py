@@ -38,6 +38,6 @@ for _ in range(a.solves):
     print(f"{desc} [{a.slabs} slab(s)]: iterations={it.value} relres={fr.value:.3e} pcg={sec.value * 1e3:.2f} ms "
           f"({sec.value * 1e3 / max(it.value, 1):.3f} ms/iteration)", flush=True)
 if a.kernels:
-    for w, name in ((0, "K.u"), (1, "sweep")):
+    for w, name in ((0, "K.u"), (1, "sweep"), (2, "update+2 sweeps")):
         ms, by = ops.time_kernel(w, a.kernels)
         print(f"{name}: {ms * 1e3:.1f} us  {by / ms / 1e6:.0f} GB/s", flush=True)
