@@ -22,7 +22,7 @@ CSRC = PKG / "csrc"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["tmg_gpu.cu", "tmg_inputs.cpp"]
-DEPS = SOURCES + ["tmg_device.cuh", "tmg_kernels.cuh", "tmg_march.cuh", "tmg_smarch.cuh", "tmg_stile.cuh", "tmg_oc.cuh", "tmg_poisson.cuh"]
+DEPS = SOURCES + ["tmg_device.cuh", "tmg_kernels.cuh", "tmg_march.cuh", "tmg_smarch.cuh", "tmg_smarch2.cuh", "tmg_stile.cuh", "tmg_oc.cuh", "tmg_poisson.cuh"]
 
 
 def _stale(target: pathlib.Path, deps) -> bool:

@@ -37,6 +37,7 @@
 #include "tmg_kernels.cuh"
 #include "tmg_march.cuh"
 #include "tmg_smarch.cuh"
+#include "tmg_smarch2.cuh"
 #include "tmg_stile.cuh"
 #include "tmg_oc.cuh"
 
@@ -401,6 +402,9 @@ struct tmg_gpu_handle {
   // coarse levels up to this many nodes run the V(2,2) halves as shared-memory
   // tiles instead of marching kernels (tmg_stile.cuh)
   long stile_max_nodes = kTileMaxNodes;
+  // two-stage coarse kernels with stage A and stage B on separate warps
+  // (tmg_smarch2.cuh; TMG_SMARCH_LOCKSTEP=1 runs the lockstep k_smarch)
+  bool smarch_split = true;
   // instrumentation
   long launches = 0;
   bool capturing = false;
@@ -976,13 +980,17 @@ void launch_smarch(H* h, Rank& R, int l, const double2* x2, const double2* uc, d
   size_t sm;
   if (!UP) {
     sm = static_cast<size_t>(kSSlotDown) * s_stages<false>();
-    const int slots = device_slots(reinterpret_cast<const void*>(k_smarch<false>), kSThreads, sm);
+    const int slots = h->smarch_split
+                          ? device_slots(reinterpret_cast<const void*>(k_smarch2<false>), kS2Threads, sm)
+                          : device_slots(reinterpret_cast<const void*>(k_smarch<false>), kSThreads, sm);
     const long ty = (a.gc.ny + 1 + (kSY - 4) / 2 - 1) / ((kSY - 4) / 2);
     a.tx = march_tx(ty, a.gc.ncol, slots, 2, 7);
     grid = dim3(ty, (a.gc.ncol + a.tx - 1) / a.tx);
   } else {
     sm = static_cast<size_t>(kSSlotUp) * s_stages<true>();
-    const int slots = device_slots(reinterpret_cast<const void*>(k_smarch<true>), kSThreads, sm);
+    const int slots = h->smarch_split
+                          ? device_slots(reinterpret_cast<const void*>(k_smarch2<true>), kS2Threads, sm)
+                          : device_slots(reinterpret_cast<const void*>(k_smarch<true>), kSThreads, sm);
     const long ty = (a.g.ny + 1 + (kSY - 2) - 1) / (kSY - 2);
     // even: CTA column ranges start on even columns
     a.tx = march_tx(ty, a.g.ncol, slots, 1, 7, true);
@@ -993,6 +1001,8 @@ void launch_smarch(H* h, Rank& R, int l, const double2* x2, const double2* uc, d
     grid = UP ? dim3((a.g.ny + kTU) / kTU, (a.g.ncol + kTU - 1) / kTU)
               : dim3((a.gc.ny + kTC) / kTC, (a.gc.ncol + kTC - 1) / kTC);
     k_stile<UP><<<grid, kTThreads, t_smem<UP>(), h->stream>>>(a);
+  } else if (h->smarch_split) {
+    k_smarch2<UP><<<grid, kS2Threads, sm, h->stream>>>(a);
   } else {
     k_smarch<UP><<<grid, kSThreads, sm, h->stream>>>(a);
   }
@@ -1794,6 +1804,10 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
                           static_cast<int>(kSSlotDown * s_stages<false>())));
   CK(cudaFuncSetAttribute(k_smarch<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(kSSlotUp * s_stages<true>())));
+  CK(cudaFuncSetAttribute(k_smarch2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(kSSlotDown * s_stages<false>())));
+  CK(cudaFuncSetAttribute(k_smarch2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(kSSlotUp * s_stages<true>())));
   CK(cudaFuncSetAttribute(k_stile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<false>()));
   CK(cudaFuncSetAttribute(k_stile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<true>()));
   CK(cudaFuncSetAttribute(k_march<StSweep01U, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1805,6 +1819,7 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
   if (const char* v = std::getenv("TMG_NO_DEVICE_LOOP")) hp->device_loop = std::atoi(v) == 0;
   if (const char* v = std::getenv("TMG_DENSE_COARSE_FACTOR")) hp->band_factor = std::atoi(v) == 0;
   if (const char* v = std::getenv("TMG_NCCL_COND_NODES")) hp->nccl_cond = std::atoi(v) != 0;
+  if (const char* v = std::getenv("TMG_SMARCH_LOCKSTEP")) hp->smarch_split = std::atoi(v) == 0;
   for (cudaEvent_t& e : hp->ev) CK(cudaEventCreate(&e));
   for (int i = 0; i < nlocal; ++i) {
     hp->own.push_back(std::make_unique<Rank>());

@@ -446,6 +446,34 @@ def test_tile_kernels_match_marching(monkeypatch, nx, ny, nc, recipe, gamma):
     assert np.array_equal(va, vc)
 
 
+@pytest.mark.parametrize("nx,ny,nc,recipe,gamma", [(64, 64, 3, "iid", 1), (256, 128, 5, "checker", 1),
+                                                   (96, 160, 4, "iid", 2), (1024, 512, 7, "iid", 1)])
+def test_specialised_coarse_kernels_are_bitwise(monkeypatch, nx, ny, nc, recipe, gamma):
+    """The two-stage coarse kernels with stage A and stage B on separate warps
+    (tmg_smarch2.cuh) perform the lockstep kernels' per-node arithmetic in the
+    same order: every result is bitwise that of TMG_SMARCH_LOCKSTEP=1. The
+    marching kernels run on every coarse level (TMG_STILE_MAX_NODES=0)."""
+    monkeypatch.setenv("TMG_STILE_MAX_NODES", "0")
+    _, E = moduli(nx, ny, recipe, 5)
+    g = P.GridLevel(nx, ny)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    b = P.assemble_rhs(g, bc)
+    cfg = P.SolverConfig(tol=1e-10, max_iter=500, gamma=gamma)
+    f = np.random.default_rng(4).standard_normal(b.size)
+    reps = []
+    for lockstep in ("0", "1"):
+        monkeypatch.setenv("TMG_SMARCH_LOCKSTEP", lockstep)
+        ops = P.MultigridOperators(g, nc, 0.3, bc)
+        ops.set_moduli(E, 0.6)
+        rep = P.pcgmg_solve(ops, b, cfg)
+        reps.append((rep, P.compliance(ops), P.mg_cycle(ops, np.zeros_like(f), f, gamma=gamma)))
+    (a, ca, va), (c, cc, vc) = reps
+    assert a.converged and a.iterations == c.iterations
+    assert a.residual_history == c.residual_history
+    assert np.array_equal(a.solution, c.solution) and ca == cc
+    assert np.array_equal(va, vc)
+
+
 @pytest.mark.parametrize("nx,ny,nc", [(64, 64, 3), (128, 96, 3), (160, 96, 4)])
 def test_banded_coarsest_factor_is_the_dense_one(monkeypatch, nx, ny, nc):
     """The banded one-warp Cholesky of the coarsest matrix performs, inside
