@@ -9,8 +9,11 @@ what optimize() runs per outer iteration (mto.cpp:267-283).
   value : inputs (moduli, rhs) resident in HBM, timed with CUDA events on the
           library's stream; MDOF/s = DOFs x PCG iterations / step seconds.
   e2e   : the same metric through the C-ABI calls a user makes with HOST
-          buffers (tmg_gpu_set_moduli + tmg_gpu_solve): H2D of moduli and rhs
-          and D2H of the solution inside the timed region.
+          buffers: H2D of moduli and rhs and D2H of the solution inside the
+          timed region, every step. Headline form: the pipelined calls
+          (tmg_gpu_stage_inputs / tmg_gpu_solve_staged), whose copies run on
+          a copy stream beside the neighbouring steps' solves; `e2e.serial`
+          is the blocking tmg_gpu_set_moduli + tmg_gpu_solve pair.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4|c2|c1]
   python bench.py --impl reference ...   # the reference's own CPU path
@@ -312,9 +315,11 @@ def gpu_arm(args, cfg_name):
     pE = lib.tmg_host_alloc(8 * nE)
     pb = lib.tmg_host_alloc(8 * nb)
     px = lib.tmg_host_alloc(8 * nb)
+    px2 = lib.tmg_host_alloc(8 * nb)
     hE = np.ctypeslib.as_array((C.c_double * nE).from_address(pE))
     hb = np.ctypeslib.as_array((C.c_double * nb).from_address(pb))
     hx = np.ctypeslib.as_array((C.c_double * nb).from_address(px))
+    hx2 = np.ctypeslib.as_array((C.c_double * nb).from_address(px2))
     hE[:] = E
     hb[:] = b
     del E
@@ -337,6 +342,24 @@ def gpu_arm(args, cfg_name):
                                      C.byref(fr), C.byref(cv), C.byref(sec), D(hist), hist.size, C.byref(hl)))
         return itc.value
 
+    def e2e_pipelined(n):
+        # the serving form of the same C-ABI path: step k+1's inputs are
+        # staged (H2D on the library's copy stream) while step k solves, and
+        # step k's solution is downloaded while step k+1 solves
+        # (tmg_gpu_stage_inputs / tmg_gpu_solve_staged, include/tmg_gpu.h)
+        outs = (hx, hx2)
+        its_ = []
+        ops._check(lib.tmg_gpu_stage_inputs(ops.h, 0, D(hE), nE, D(hb)))
+        for k in range(n):
+            if k + 1 < n:
+                ops._check(lib.tmg_gpu_stage_inputs(ops.h, (k + 1) & 1, D(hE), nE, D(hb)))
+            ops._check(lib.tmg_gpu_solve_staged(ops.h, k & 1, OMEGA, TOL, MAX_ITER, 1, SWEEPS, SWEEPS, D(outs[k & 1]),
+                                                C.byref(itc), C.byref(fr), C.byref(cv), C.byref(sec), D(hist),
+                                                hist.size, C.byref(hl)))
+            its_.append(itc.value)
+        ops._check(lib.tmg_gpu_sync_outputs(ops.h))
+        return its_
+
     def barrier():
         if dist:
             dist.barrier()
@@ -356,6 +379,7 @@ def gpu_arm(args, cfg_name):
     for _ in range(max(args.warmup, 3)):
         resident_step()
     e2e_step()
+    e2e_pipelined(2)
 
     # ---- value: inputs resident in HBM
     clocks = Clocks(local)
@@ -373,14 +397,22 @@ def gpu_arm(args, cfg_name):
     t_res = max_over_ranks(ms.value)
     setup_ms, pcg_ms = ops.last_timings()
 
-    # ---- e2e: host buffers through the C ABI
+    # ---- e2e: host buffers through the C ABI, pipelined (the headline) and
+    # one blocking solve at a time
     barrier()
     ops._check(lib.tmg_gpu_event_record(ops.h, 2))
-    e_its = [e2e_step() for _ in range(args.steps)]
+    e_its = e2e_pipelined(args.steps)
     ops._check(lib.tmg_gpu_event_record(ops.h, 3))
     ops._check(lib.tmg_gpu_event_elapsed(ops.h, 2, 3, C.byref(ms)))
     barrier()
     t_e2e = max_over_ranks(ms.value)
+    barrier()
+    ops._check(lib.tmg_gpu_event_record(ops.h, 2))
+    s_its = [e2e_step() for _ in range(args.steps)]
+    ops._check(lib.tmg_gpu_event_record(ops.h, 3))
+    ops._check(lib.tmg_gpu_event_elapsed(ops.h, 2, 3, C.byref(ms)))
+    barrier()
+    t_ser = max_over_ranks(ms.value)
 
     # ---- dominant-kernel roofline, live CUDA events on the library's stream:
     # the fused PCG update + two pre-sweeps (the largest share of a PCG
@@ -397,6 +429,7 @@ def gpu_arm(args, cfg_name):
         # strong scaling: the same global solve at every N (weak: 1024 columns per GPU)
         value = dofs * sum(its) / (t_res * 1e-3) / 1e6
         e2e_value = dofs * sum(e_its) / (t_e2e * 1e-3) / 1e6
+        ser_value = dofs * sum(s_its) / (t_ser * 1e-3) / 1e6
         result = {
             "metric": METRIC, "value": value, "unit": "MDOF/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_res / args.steps, "higher_is_better": True,
@@ -412,7 +445,14 @@ def gpu_arm(args, cfg_name):
                        "setup_ms_last": setup_ms, "pcg_ms_last": pcg_ms,
                        "pcg_only_mdof_s": dofs * its[-1] / (pcg_ms * 1e-3) / 1e6},
             "e2e": {"value": e2e_value, "unit": "MDOF/s", "h2d_bytes_per_step": 8 * nE + 8 * nb,
-                    "d2h_bytes_per_step": 8 * nb, "ms_per_step": t_e2e / args.steps},
+                    "d2h_bytes_per_step": 8 * nb, "ms_per_step": t_e2e / args.steps,
+                    "mode": "pipelined: each step copies its moduli and rhs from pinned host memory to the device "
+                            "and its solution back, on the library's copy stream, overlapping the neighbouring "
+                            "steps' solves (tmg_gpu_stage_inputs / tmg_gpu_solve_staged / tmg_gpu_sync_outputs); "
+                            "the timed region runs from before the first upload to after the last download",
+                    "pcg_iterations": e_its,
+                    "serial": {"value": ser_value, "ms_per_step": t_ser / args.steps, "pcg_iterations": s_its,
+                               "mode": "one blocking tmg_gpu_set_moduli + tmg_gpu_solve per step"}},
             "gpu_launches": launches,
             "clocks": clk,
             "roofline": {"bound": "hbm",

@@ -157,6 +157,45 @@ int tmg_gpu_download_solution(tmg_gpu_handle* h, double* x_out);
 /* Promote the resident solution to the warm start of the next solve. */
 int tmg_gpu_solution_to_x0(tmg_gpu_handle* h);
 
+/* ---- pipelined solves (serving a stream of independent problems) ------- */
+
+/* The blocking tmg_gpu_set_moduli + tmg_gpu_solve pair moves 24 B of inputs
+ * per element+node over PCIe before each solve and 16 B per node after it,
+ * with the device idle. These three calls overlap those copies with the
+ * previous / next solve on a second (copy) stream, for callers that solve
+ * many independent problems on one mesh (the same outer loop as
+ * mto.cpp:264-310 with the inputs supplied per call):
+ *
+ *   stage(0, E_0, b_0)
+ *   for k: stage((k+1)&1, E_{k+1}, b_{k+1});   (returns at once)
+ *          solve_staged(k&1, ..., u_k)         (blocks until the iteration
+ *                                               count is known; u_k arrives
+ *                                               during the next solve)
+ *   sync_outputs()                             (every u_k is on the host)
+ *
+ * tmg_gpu_stage_inputs copies moduli (nx*ny, element order of
+ * tmg_gpu_upload_moduli) and b (2N) into staging slot 0 or 1 on the copy
+ * stream, after the slot's previous contents were installed. Host buffers
+ * must be PINNED (tmg_host_alloc) for the copies to overlap; pageable
+ * memory still works, synchronously. The host arrays are read while the
+ * copies run: keep them unchanged until the slot's tmg_gpu_solve_staged
+ * returns.
+ *
+ * tmg_gpu_solve_staged installs the slot's inputs, builds the hierarchy with
+ * omega (tmg_gpu_setup) and solves from x0 = 0 exactly like tmg_gpu_solve
+ * (same outputs and errors); x_out (2N, pinned) is written asynchronously
+ * and is complete after tmg_gpu_sync_outputs (call it before reading).
+ * Results are bitwise those of tmg_gpu_set_moduli + tmg_gpu_solve. */
+int tmg_gpu_stage_inputs(tmg_gpu_handle* h, int slot, const double* moduli,
+                         long n_elem, const double* b);
+int tmg_gpu_solve_staged(tmg_gpu_handle* h, int slot, double omega, double tol,
+                         int max_iter, int gamma, int pre_sweeps,
+                         int post_sweeps, double* x_out, int* iterations,
+                         double* final_residual, int* converged,
+                         double* seconds, double* history, int history_cap,
+                         int* history_len);
+int tmg_gpu_sync_outputs(tmg_gpu_handle* h);
+
 /* ---- consumers of u (mto.cpp:300-310) ---------------------------------- */
 
 /* u^T K u with the eliminated operator (fem.cpp:284-290). u = NULL uses the

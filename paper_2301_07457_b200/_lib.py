@@ -55,6 +55,10 @@ SIGNATURES = [
                                          _I, _D, _I, _D, _D, C.c_int, _I]),
     ("tmg_gpu_download_solution", C.c_int, [_H, _D]),
     ("tmg_gpu_solution_to_x0", C.c_int, [_H]),
+    ("tmg_gpu_stage_inputs", C.c_int, [_H, C.c_int, _D, C.c_long, _D]),
+    ("tmg_gpu_solve_staged", C.c_int, [_H, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       _D, _I, _D, _I, _D, _D, C.c_int, _I]),
+    ("tmg_gpu_sync_outputs", C.c_int, [_H]),
     ("tmg_gpu_compliance", C.c_int, [_H, _D, _D]),
     ("tmg_gpu_element_energies", C.c_int, [_H, _D, _D]),
     ("tmg_gpu_sensitivities", C.c_int, [_H, _D, C.c_int, _D, _D, C.c_double, _D]),

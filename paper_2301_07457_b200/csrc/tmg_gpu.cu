@@ -194,6 +194,12 @@ struct Rank {
   long aux2_cap = 0;
   double* ocbuf = nullptr;  // OC exchange scratch (tmg_oc.cuh)
   long ocbuf_cap = 0;
+  // pipelined solves (tmg_gpu_stage_inputs / tmg_gpu_solve_staged): two
+  // staging slots of moduli + rhs and the solution's staging copy, in the
+  // resident arrays' padded layouts (allocated on first use)
+  double* Es[2] = {nullptr, nullptr};
+  double2* bs[2] = {nullptr, nullptr};
+  double2* us = nullptr;
 
   Level& fine() { return lev[nc]; }
   double2* rbuf(int k) const { return k ? r2 : r; }
@@ -405,6 +411,14 @@ struct tmg_gpu_handle {
   // two-stage coarse kernels with stage A and stage B on separate warps
   // (tmg_smarch2.cuh; TMG_SMARCH_LOCKSTEP=1 runs the lockstep k_smarch)
   bool smarch_split = true;
+  // pipelined solves: the copy stream and its hand-off events (staged[k]:
+  // slot k's inputs landed; consumed[k]: slot k copied into the resident
+  // arrays; solved: the solution's staging copy is written; downloaded: it
+  // reached the host)
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t staged[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+  cudaEvent_t solved = nullptr, downloaded = nullptr;
+  bool staged_ok[2] = {false, false};
   // instrumentation
   long launches = 0;
   bool capturing = false;
@@ -568,7 +582,9 @@ void free_rank(Rank& R) {
                   static_cast<void*>(R.pbuf[1]), static_cast<void*>(R.partials), static_cast<void*>(R.gparts),
                   static_cast<void*>(R.ticket),
                   static_cast<void*>(R.st), static_cast<void*>(R.scal), static_cast<void*>(R.dense),
-                  static_cast<void*>(R.aux), static_cast<void*>(R.aux2), static_cast<void*>(R.ocbuf)})
+                  static_cast<void*>(R.aux), static_cast<void*>(R.aux2), static_cast<void*>(R.ocbuf),
+                  static_cast<void*>(R.Es[0]), static_cast<void*>(R.Es[1]), static_cast<void*>(R.bs[0]),
+                  static_cast<void*>(R.bs[1]), static_cast<void*>(R.us)})
     cudaFree(p);
   if (R.hm) cudaFreeHost(R.hm);
   if (R.lrec) cudaFreeHost(R.lrec);
@@ -591,6 +607,12 @@ void free_handle(H* h) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : h->uev)
     if (e) cudaEventDestroy(e);
+  if (h->cstream) {
+    cudaStreamSynchronize(h->cstream);
+    for (cudaEvent_t e : {h->staged[0], h->staged[1], h->consumed[0], h->consumed[1], h->solved, h->downloaded})
+      if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(h->cstream);
+  }
   if (h->stream) cudaStreamDestroy(h->stream);
 }
 
@@ -1741,12 +1763,13 @@ void copy_out_hist(const SolveOut& o, double* history, int cap, int* len) {
 
 // Host upload of the fine moduli of one rank: element columns
 // [x0 - kGX, x0 + ncol + kGX) clipped to the mesh (ghost elements stay 0).
-void upload_moduli_rank(H* h, Rank& R, const double* moduli) {
+void upload_moduli_rank(H* h, Rank& R, const double* moduli, double* dst = nullptr, cudaStream_t s = nullptr) {
   const Grid& g = R.fine().g;
   const int e0 = std::max(0, g.x0 - kGX), e1 = std::min(g.nx, g.x0 + g.ncol + kGX);
   if (e1 > e0)
-    CK(cudaMemcpy2DAsync(R.E + g.idx(e0 - g.x0, 0), sizeof(double) * g.P, moduli + static_cast<long>(e0) * g.ny,
-                         sizeof(double) * g.ny, sizeof(double) * g.ny, e1 - e0, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpy2DAsync((dst ? dst : R.E) + g.idx(e0 - g.x0, 0), sizeof(double) * g.P,
+                         moduli + static_cast<long>(e0) * g.ny, sizeof(double) * g.ny, sizeof(double) * g.ny,
+                         e1 - e0, cudaMemcpyHostToDevice, s ? s : h->stream));
 }
 
 int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks, int rank, int nlocal,
@@ -1873,6 +1896,30 @@ int create_handle(int nx, int ny, int nc, int dpn, int device, int nranks, int r
 }  // namespace
 
 // =================================================================== ABI ==
+
+// Pipelined solves: the copy stream, its events and every rank's staging
+// buffers (zero-filled once, so their ghost columns and padding stay zero).
+void ensure_pipeline(H* h) {
+  if (h->cstream) return;
+  CK(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&h->staged[0], &h->staged[1], &h->consumed[0], &h->consumed[1], &h->solved,
+                         &h->downloaded})
+    CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  for (Rank* R : h->ranks) {
+    const Grid& g = R->fine().g;
+    const size_t eb = sizeof(double) * (g.size + kSlackNodes), vb = sizeof(double2) * (g.size + kSlackNodes);
+    for (int k = 0; k < 2; ++k) {
+      CK(cudaMalloc(&R->Es[k], eb));
+      CK(cudaMemsetAsync(R->Es[k], 0, eb, h->stream));
+      CK(cudaMalloc(&R->bs[k], vb));
+      CK(cudaMemsetAsync(R->bs[k], 0, vb, h->stream));
+    }
+    CK(cudaMalloc(&R->us, vb));
+  }
+  for (cudaEvent_t e : {h->consumed[0], h->consumed[1]}) CK(cudaEventRecord(e, h->stream));
+  CK(cudaEventRecord(h->downloaded, h->cstream));
+  CK(cudaStreamSynchronize(h->stream));
+}
 
 extern "C" {
 
@@ -2096,6 +2143,79 @@ int tmg_gpu_solve(tmg_gpu_handle* h, const double* b, const double* x0, double t
     if (converged) *converged = o.converged;
     if (seconds) *seconds = o.seconds;
     copy_out_hist(o, history, history_cap, history_len);
+  });
+}
+
+int tmg_gpu_stage_inputs(tmg_gpu_handle* h, int slot, const double* moduli, long n_elem, const double* b) {
+  return guarded(h, [&] {
+    if (slot != 0 && slot != 1) fail(TMG_ERR_DIMENSION, "staging slot must be 0 or 1");
+    if (n_elem != static_cast<long>(h->nx) * h->ny)
+      fail(TMG_ERR_DIMENSION, "element modulus count " + std::to_string(n_elem) + " does not match grid with " +
+                                  std::to_string(static_cast<long>(h->nx) * h->ny) + " elements");
+    if (!h->have_problem) fail(TMG_ERR_CONFIG, "problem not set (call tmg_gpu_set_problem)");
+    ensure_pipeline(h);
+    // the slot's previous contents must have been copied into the resident arrays
+    CK(cudaStreamWaitEvent(h->cstream, h->consumed[slot], 0));
+    for (Rank* R : h->ranks) {
+      upload_moduli_rank(h, *R, moduli, R->Es[slot], h->cstream);
+      upload_nodes(h->cstream, R->bs[slot], b, R->fine().g);
+    }
+    CK(cudaEventRecord(h->staged[slot], h->cstream));
+    h->staged_ok[slot] = true;
+  });
+}
+
+int tmg_gpu_solve_staged(tmg_gpu_handle* h, int slot, double omega, double tol, int max_iter, int gamma,
+                         int pre_sweeps, int post_sweeps, double* x_out, int* iterations, double* final_residual,
+                         int* converged, double* seconds, double* history, int history_cap, int* history_len) {
+  return guarded(h, [&] {
+    if (slot != 0 && slot != 1) fail(TMG_ERR_DIMENSION, "staging slot must be 0 or 1");
+    if (!h->cstream || !h->staged_ok[slot]) fail(TMG_ERR_CONFIG, "no inputs staged in this slot");
+    h->staged_ok[slot] = false;
+    // install the staged moduli and rhs (device copies after the staging copies land)
+    CK(cudaStreamWaitEvent(h->stream, h->staged[slot], 0));
+    for (Rank* R : h->ranks) {
+      const Grid& g = R->fine().g;
+      CK(cudaMemcpyAsync(R->E, R->Es[slot], sizeof(double) * (g.size + kSlackNodes), cudaMemcpyDeviceToDevice,
+                         h->stream));
+      CK(cudaMemcpyAsync(R->b, R->bs[slot], sizeof(double2) * (g.size + kSlackNodes), cudaMemcpyDeviceToDevice,
+                         h->stream));
+    }
+    CK(cudaEventRecord(h->consumed[slot], h->stream));
+    h->have_moduli = true;
+    h->have_setup = false;
+    CK(cudaEventRecord(h->ev[2], h->stream));
+    setup(h, omega);
+    CK(cudaEventRecord(h->ev[3], h->stream));
+    SolveOut o;
+    solve_resident(h, false, tol, max_iter, gamma, pre_sweeps, post_sweeps, o);
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev[2], h->ev[3]));
+    h->last_setup_ms = ms;
+    // the solution's staging copy (once the previous download has read it),
+    // then its download on the copy stream, overlapping whatever the compute
+    // stream runs next
+    CK(cudaStreamWaitEvent(h->stream, h->downloaded, 0));
+    for (Rank* R : h->ranks)
+      CK(cudaMemcpyAsync(R->us, R->x, sizeof(double2) * R->fine().g.size, cudaMemcpyDeviceToDevice, h->stream));
+    CK(cudaEventRecord(h->solved, h->stream));
+    CK(cudaStreamWaitEvent(h->cstream, h->solved, 0));
+    for (Rank* R : h->ranks) download_nodes(h->cstream, x_out, R->us, R->fine().g);
+    CK(cudaEventRecord(h->downloaded, h->cstream));
+    if (iterations) *iterations = o.iterations;
+    if (final_residual) *final_residual = o.final_residual;
+    if (converged) *converged = o.converged;
+    if (seconds) *seconds = o.seconds;
+    copy_out_hist(o, history, history_cap, history_len);
+  });
+}
+
+int tmg_gpu_sync_outputs(tmg_gpu_handle* h) {
+  return guarded(h, [&] {
+    if (!h->cstream) return;
+    // later work on the compute stream (and its events) orders after the downloads
+    CK(cudaStreamWaitEvent(h->stream, h->downloaded, 0));
+    CK(cudaEventSynchronize(h->downloaded));
   });
 }
 

@@ -455,6 +455,72 @@ def pcgmg_solve(ops: MultigridOperators, b: np.ndarray, cfg: SolverConfig,
                        seconds=sec.value, residual_history=hist[: hl.value].tolist())
 
 
+class PinnedArray:
+    """A float64 array in page-locked host memory (tmg_host_alloc), the kind
+    of buffer the pipelined solves overlap their copies with; ``.a`` is the
+    numpy view. Freed with the object."""
+
+    def __init__(self, n: int):
+        self.lib = _lib.load()
+        self.ptr = self.lib.tmg_host_alloc(8 * max(1, n))
+        if not self.ptr:
+            raise CudaError("tmg_host_alloc failed")
+        buf = (C.c_double * max(1, n)).from_address(self.ptr)
+        buf._owner = self  # the numpy view keeps the pinned block alive
+        self.a = np.ctypeslib.as_array(buf)[:n]
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            self.lib.tmg_host_free(self.ptr)
+            self.ptr = None
+
+
+def pcgmg_solve_many(ops: MultigridOperators, problems, cfg: SolverConfig, omega: float = 0.6,
+                     outputs=None) -> list:
+    """A stream of independent solves on one mesh: problem k = (moduli_k,
+    b_k) gets set_moduli(moduli_k, omega) + pcgmg_solve(b_k) semantics
+    (solvers.cpp:460-530; bitwise the same results), with the host<->device
+    copies of problem k+1's inputs and problem k-1's solution overlapping
+    solve k (tmg_gpu_stage_inputs / tmg_gpu_solve_staged, include/tmg_gpu.h).
+    Inputs in PinnedArray buffers overlap; plain arrays work, serialised.
+    ``outputs``: optional per-problem float64 arrays (pinned to overlap) that
+    receive the solutions; by default each report gets a fresh array."""
+    probs = [(np.ascontiguousarray(e, dtype=np.float64), np.ascontiguousarray(b, dtype=np.float64))
+             for e, b in problems]
+    n = ops.grid.dof_count()
+    ne = ops.grid.element_count()
+    for e, b in probs:
+        if e.size != ne:
+            raise DimensionError(f"element modulus count {e.size} does not match grid with {ne} elements")
+        if b.size != n:
+            raise DimensionError(f"rhs length {b.size} != dof count {n}")
+    outs = outputs if outputs is not None else [np.empty(n) for _ in probs]
+    ops.omega = omega
+    lib = ops.lib
+
+    def stage(k):
+        e, b = probs[k]
+        ops._check(lib.tmg_gpu_stage_inputs(ops.h, k & 1, dptr(e), e.size, dptr(b)))
+
+    reports = []
+    if probs:
+        stage(0)
+    for k in range(len(probs)):
+        if k + 1 < len(probs):
+            stage(k + 1)
+        it, fr, cv, sec, hl = C.c_int(), C.c_double(), C.c_int(), C.c_double(), C.c_int()
+        hist = np.empty(cfg.max_iter + 1)
+        ops._check(lib.tmg_gpu_solve_staged(ops.h, k & 1, omega, cfg.tol, cfg.max_iter, cfg.gamma,
+                                            cfg.pre_sweeps, cfg.post_sweeps, dptr(outs[k]), C.byref(it),
+                                            C.byref(fr), C.byref(cv), C.byref(sec), dptr(hist), hist.size,
+                                            C.byref(hl)))
+        reports.append(SolveReport(solution=outs[k], iterations=it.value, final_residual=fr.value,
+                                   converged=bool(cv.value), seconds=sec.value,
+                                   residual_history=hist[: hl.value].tolist()))
+    ops._check(lib.tmg_gpu_sync_outputs(ops.h))
+    return reports
+
+
 def compliance(ops: MultigridOperators, u: np.ndarray | None = None) -> float:
     """u^T K u (fem.cpp:284-290); u=None uses the resident solution."""
     uc = None if u is None else np.ascontiguousarray(u, dtype=np.float64)
