@@ -36,13 +36,19 @@
 
 namespace tmg {
 
-constexpr int kSY = 96;                 // consumer threads (rows) per CTA
+#ifndef TMG_SY
+#define TMG_SY 96
+#endif
+constexpr int kSY = TMG_SY;             // consumer threads (rows) per CTA (per stage group in k_smarch2)
 constexpr int kSWarps = kSY / 32;
 constexpr int kSThreads = kSY + 32;     // + one producer warp
 // ring depth: 4 resident columns + 2 in flight, the most that keeps two
 // CTAs per SM
+#ifndef TMG_SSTAGES
+#define TMG_SSTAGES 6
+#endif
 template <bool UP>
-__host__ __device__ constexpr int s_stages() { return 6; }
+__host__ __device__ constexpr int s_stages() { return TMG_SSTAGES; }
 constexpr int kSRows = kSY + 2;         // streamed rows per column
 // every coarse level runs the two-stage V(2,2) halves (measured on c1-c4:
 // one-pass kernels for the small levels were 1-13 % slower per PCG
