@@ -115,6 +115,7 @@ struct NcclApi {
   decltype(&ncclCommDestroy) commDestroy = nullptr;
   decltype(&ncclAllReduce) allReduce = nullptr;
   decltype(&ncclBroadcast) broadcast = nullptr;
+  decltype(&ncclAllGather) allGather = nullptr;
   decltype(&ncclSend) send = nullptr;
   decltype(&ncclRecv) recv = nullptr;
   decltype(&ncclGroupStart) groupStart = nullptr;
@@ -134,6 +135,7 @@ const NcclApi& nccl() {
       api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(lib, "ncclCommDestroy"));
       api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(lib, "ncclAllReduce"));
       api.broadcast = reinterpret_cast<decltype(api.broadcast)>(dlsym(lib, "ncclBroadcast"));
+      api.allGather = reinterpret_cast<decltype(api.allGather)>(dlsym(lib, "ncclAllGather"));
       api.send = reinterpret_cast<decltype(api.send)>(dlsym(lib, "ncclSend"));
       api.recv = reinterpret_cast<decltype(api.recv)>(dlsym(lib, "ncclRecv"));
       api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(lib, "ncclGroupStart"));
@@ -330,12 +332,32 @@ struct NcclComm : Comm {
     Rank& me = *rs[0];
     const long P = me.lev[level].g.P;
     char* buf = static_cast<char*>(field(me));
+    // The partition gives every rank the same column count but the last one
+    // (which also holds column nx): one in-place all-gather of that common
+    // count per plane, plus one broadcast of the last rank's extra columns.
+    // Any other layout: one broadcast per rank and plane.
+    const int cmin = ncol[0];
+    bool uniform = nccl().allGather != nullptr && ncol[nranks - 1] >= cmin;
+    for (int r = 0; r < nranks; ++r)
+      uniform = uniform && X0[r] == X0[0] + r * cmin && (r == nranks - 1 || ncol[r] == cmin);
     NK(nccl().groupStart());
-    for (int src = 0; src < nranks; ++src)
-      for (int k = 0; k < planes; ++k) {
-        char* p = buf + (k * plane_stride + static_cast<long>(X0[src] + kGX) * P) * esize;
-        NK(nccl().broadcast(p, p, ncol[src] * P * esize, ncclChar, src, comm, s));
+    for (int k = 0; k < planes; ++k) {
+      char* p0 = buf + (k * plane_stride + static_cast<long>(X0[0] + kGX) * P) * esize;
+      if (uniform) {
+        const size_t cnt = static_cast<size_t>(cmin) * P * esize;
+        NK(nccl().allGather(p0 + rank * cnt, p0, cnt, ncclChar, comm, s));
+        const int extra = ncol[nranks - 1] - cmin;
+        if (extra > 0) {
+          char* pe = p0 + static_cast<size_t>(nranks) * cnt;
+          NK(nccl().broadcast(pe, pe, static_cast<size_t>(extra) * P * esize, ncclChar, nranks - 1, comm, s));
+        }
+      } else {
+        for (int src = 0; src < nranks; ++src) {
+          char* p = buf + (k * plane_stride + static_cast<long>(X0[src] + kGX) * P) * esize;
+          NK(nccl().broadcast(p, p, ncol[src] * P * esize, ncclChar, src, comm, s));
+        }
       }
+    }
     NK(nccl().groupEnd());
   }
   void allreduce(std::vector<Rank*>& rs, int len, cudaStream_t s) override {

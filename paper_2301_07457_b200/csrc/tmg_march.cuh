@@ -34,6 +34,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "tmg_device.cuh"
@@ -554,26 +555,49 @@ struct StProlongSweep : WithF<0> {
     v[1] = odd ? h12 : c1;
     v[2] = odd ? c2 : h12;
   }
-  __device__ static void load(const MarchArgs&, const unsigned char* s, const unsigned char* ps,
-                              const int* mis, int t, int c, Col& col) {
+  // The interpolated coarse column of the last loaded entry: entries 2X-1,
+  // 2X and 2X+1 all use coarse column X (as ceil(c/2) for the first two, as
+  // floor(c/2) for the odd 2X+1), so each is interpolated once per thread
+  // instead of three times (same values: the same coarse data and formula).
+  struct Carry {
+    double2 v[3];
+    int col = -0x40000000;
+  };
+  __device__ static void load(const MarchArgs&, const unsigned char* s, const unsigned char*, const int* mis,
+                              int t, int c, Col& col, Carry& cy) {
     load_window(s, O_U, O_E, O_M, mis, t, col);
+    const bool have = (cy.col == c - 1);
     double2 cur[3];
-    rows_of(s, mis, t, cur);
     if (c & 1) {
+      // odd: the mean of coarse columns (c-1)/2 (the previous entry's) and (c+1)/2
       double2 prv[3] = {};
-      if (ps) rows_of(ps, mis, t, prv);
+      if (have) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) prv[q] = cy.v[q];
+      }
+      rows_of(s, mis, t, cur);
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         col.u[q].x += 0.5 * prv[q].x + 0.5 * cur[q].x;
         col.u[q].y += 0.5 * prv[q].y + 0.5 * cur[q].y;
       }
     } else {
+      // even: coarse column c/2, which the previous (odd) entry interpolated
+      if (have) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) cur[q] = cy.v[q];
+      } else {
+        rows_of(s, mis, t, cur);
+      }
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         col.u[q].x += cur[q].x;
         col.u[q].y += cur[q].y;
       }
     }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) cy.v[q] = cur[q];
+    cy.col = c;
   }
   __device__ static void run(const MarchArgs& a, const Col& L, const Col& C, const Col& R,
                              const unsigned char* cs, const int* mis, int x, int yt, int t, bool live, double&,
@@ -621,6 +645,18 @@ struct StPupd {
 };
 
 // ------------------------------------------------------------------ kernel --
+
+// Stages may declare a `Carry` type (state carried between consecutive loads)
+template <class Stage, class = void>
+struct CarryOf {
+  struct type {};
+  static constexpr bool used = false;
+};
+template <class Stage>
+struct CarryOf<Stage, std::void_t<typename Stage::Carry>> {
+  using type = typename Stage::Carry;
+  static constexpr bool used = true;
+};
 
 // Column range of one CTA: ring entries [cf, cl]; run() is called for every
 // window centre x in [xlo, xhi] (restriction stage: every fine column it
@@ -719,13 +755,19 @@ __global__ void __launch_bounds__(kMarchThreads) k_march(MarchArgs a) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[j % kStages]);
     };
+    // per-thread state a stage carries from one loaded entry to the next
+    typename CarryOf<Stage>::type carry{};
     // load entry j into dst (needs entry j-1's slot as `prev`)
     auto fetch = [&](int j, Col& dst) {
       mbar_wait(&full[j % kStages], (j / kStages) & 1);
       const int c = cf + j;
       const unsigned char* prev = (j > 0 && in_storage(c - 1)) ? slot(j - 1) : nullptr;
-      if (in_storage(c)) Stage::load(a, slot(j), prev, mis, t, c, dst);
-      else dst = Col{};
+      if (in_storage(c)) {
+        if constexpr (CarryOf<Stage>::used) Stage::load(a, slot(j), prev, mis, t, c, dst, carry);
+        else Stage::load(a, slot(j), prev, mis, t, c, dst);
+      } else {
+        dst = Col{};
+      }
     };
     // window centred on entry j-1 (column cf + j - 1), then free its slot
     auto step = [&](const Col& L, const Col& Cc, const Col& R, int j) {
