@@ -92,6 +92,45 @@ class PcgmgGpu {
     return rep;
   }
 
+  // A stream of independent problems {(element moduli, rhs)} on this mesh:
+  // per problem set_moduli(moduli, omega) + solve(rhs, cfg) semantics and
+  // results (bitwise), with each problem's host<->device copies overlapping
+  // the neighbouring solves (tmg_gpu_stage_inputs / tmg_gpu_solve_staged,
+  // include/tmg_gpu.h). The inputs are read while their copies run; they stay
+  // untouched in the caller's vectors. Pinned memory overlaps best; std::vector
+  // storage works (serialised copies).
+  std::vector<SolveReport> solve_many(const std::vector<std::pair<std::vector<double>, std::vector<double>>>& probs,
+                                      const SolverConfig& cfg, double omega) {
+    for (const auto& p : probs) {
+      if (static_cast<int>(p.first.size()) != grid_.element_count())
+        throw DimensionError("solve_many: element modulus count does not match the grid");
+      if (static_cast<int>(p.second.size()) != grid_.dof_count())
+        throw DimensionError("pcgmg_solve: rhs length does not match the grid");
+    }
+    std::vector<SolveReport> out(probs.size());
+    auto stage = [&](size_t k) {
+      check(tmg_gpu_stage_inputs(h_, static_cast<int>(k & 1), probs[k].first.data(),
+                                 static_cast<long>(probs[k].first.size()), probs[k].second.data()));
+    };
+    if (!probs.empty()) stage(0);
+    for (size_t k = 0; k < probs.size(); ++k) {
+      if (k + 1 < probs.size()) stage(k + 1);
+      SolveReport& rep = out[k];
+      rep.solution.resize(probs[k].second.size());
+      rep.residual_history.resize(static_cast<size_t>(cfg.max_iter) + 1);
+      int iters = 0, conv = 0, hl = 0;
+      check(tmg_gpu_solve_staged(h_, static_cast<int>(k & 1), omega, cfg.tol, cfg.max_iter, cfg.gamma,
+                                 cfg.pre_sweeps, cfg.post_sweeps, rep.solution.data(), &iters, &rep.final_residual,
+                                 &conv, &rep.seconds, rep.residual_history.data(),
+                                 static_cast<int>(rep.residual_history.size()), &hl));
+      rep.iterations = iters;
+      rep.converged = conv != 0;
+      rep.residual_history.resize(static_cast<size_t>(hl));
+    }
+    check(tmg_gpu_sync_outputs(h_));
+    return out;
+  }
+
   // compliance of the resident solution (fem.cpp:284-290)
   double compliance() const {
     double c = 0.0;

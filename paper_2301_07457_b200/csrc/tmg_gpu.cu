@@ -182,6 +182,8 @@ struct Rank {
   // device-side PCG loop: its record and residual history (pinned, mapped)
   LoopRecord* lrec = nullptr;
   LoopRecord* lrec_dev = nullptr;
+  Readback* rbk = nullptr;  // mid-solve readbacks (pinned, mapped)
+  Readback* rbk_dev = nullptr;
   double* hist = nullptr;
   double* hist_dev = nullptr;
   int hist_cap = 0;
@@ -610,6 +612,7 @@ void free_rank(Rank& R) {
     cudaFree(p);
   if (R.hm) cudaFreeHost(R.hm);
   if (R.lrec) cudaFreeHost(R.lrec);
+  if (R.rbk) cudaFreeHost(R.rbk);
   if (R.hist) cudaFreeHost(R.hist);
   if (R.scal_host) cudaFreeHost(R.scal_host);
 }
@@ -715,6 +718,9 @@ void alloc_rank(H* h, Rank& R) {
   std::memset(R.hm, 0, sizeof(HostMirror));
   CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.hm_dev), R.hm, 0));
   CK(cudaHostAlloc(&R.scal_host, 4 * sizeof(double), cudaHostAllocDefault));
+  CK(cudaHostAlloc(&R.rbk, sizeof(Readback), cudaHostAllocMapped));
+  std::memset(R.rbk, 0, sizeof(Readback));
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.rbk_dev), R.rbk, 0));
   CK(cudaHostAlloc(&R.lrec, sizeof(LoopRecord), cudaHostAllocMapped));
   std::memset(R.lrec, 0, sizeof(LoopRecord));
   CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&R.lrec_dev), R.lrec, 0));
@@ -1563,9 +1569,13 @@ void setup(H* h, double omega) {
     h->count(2);
   }
   for (Rank* R : h->ranks) {
-    int bad = -1;
-    CK(cudaMemcpyAsync(&bad, R->bad_row, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-    CK(cudaStreamSynchronize(h->stream));
+    k_readback<<<1, 1, 0, h->stream>>>(R->bad_row, nullptr, nullptr, R->rbk_dev);
+    CKL();
+    h->count();
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  for (Rank* R : h->ranks) {
+    const int bad = R->rbk->bad_row;
     if (bad >= 0) {
       fail(TMG_ERR_DEFINITENESS,
            "matrix is not positive definite: non-positive pivot at row " + std::to_string(bad), bad);
@@ -1650,19 +1660,20 @@ void solve_resident(H* h, bool use_x0, double tol, int max_iter, int gamma, int 
   auto rvec = [&](Rank& R) { return R.r; };
   if (use_x0) dot(h, rvec, rvec, kRedPlain, true);
   Rank& R0 = *h->ranks[0];
-  PcgState st0;
-  CK(cudaMemcpyAsync(&st0, R0.st, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
-  CK(cudaMemcpyAsync(R0.scal_host, R0.scal, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  k_readback<<<1, 1, 0, h->stream>>>(nullptr, R0.st, R0.scal, R0.rbk_dev);
+  CKL();
+  h->count();
   CK(cudaStreamSynchronize(h->stream));
+  const double bnorm = R0.rbk->bnorm, rr0 = R0.rbk->scal0;
   o = SolveOut{};
   h->have_solution = true;
   // pcg_solve, solvers.cpp:336-357
-  if (st0.bnorm == 0.0) {
+  if (bnorm == 0.0) {
     for (Rank* R : h->ranks) CK(cudaMemsetAsync(R->x, 0, sizeof(double2) * R->fine().g.size, h->stream));
     o.converged = 1;
     o.hist.push_back(0.0);
   } else {
-    double rel = std::sqrt(*R0.scal_host) / st0.bnorm;
+    double rel = std::sqrt(rr0) / bnorm;
     o.final_residual = rel;
     o.hist.push_back(rel);
     if (rel <= tol) {

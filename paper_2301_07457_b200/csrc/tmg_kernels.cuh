@@ -60,6 +60,21 @@ struct HostMirror {
   int it;
 };
 
+// Small device values the host needs mid-solve, written by a kernel into
+// mapped pinned memory. A cudaMemcpyAsync D2H would queue behind any large
+// device-to-host copy in flight on the same copy engine (the pipelined
+// solves download the previous solution while the next one runs).
+struct Readback {
+  double bnorm;  // PcgState::bnorm
+  double scal0;  // scal[0] (the plain value of the last reduction)
+  int bad_row;   // coarsest Cholesky: first non-positive pivot, or -1
+};
+__global__ void k_readback(const int* bad_row, const PcgState* st, const double* scal, Readback* out) {
+  if (bad_row) out->bad_row = *bad_row;
+  if (st) out->bnorm = st->bnorm;
+  if (scal) out->scal0 = scal[0];
+}
+
 enum RedOp { kRedNone = 0, kRedZr = 1, kRedPap = 2, kRedRr = 3, kRedB = 4, kRedPlain = 5 };
 
 __device__ __forceinline__ void apply_scalar(RedOp op, double acc, PcgState* st, HostMirror* hm, double* out);

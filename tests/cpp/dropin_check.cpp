@@ -81,6 +81,9 @@ int main(int argc, char** argv) {
   const GridHierarchy hier = build_hierarchy(n, n, cfg.solver.num_coarsenings, 2);
   gpu::PcgmgGpu dev(prob.grid, cfg.solver.num_coarsenings, mat.poisson_ratio, prob.bc);
   int bad = 0;
+  // every design's (moduli, rhs) and blocking solution, for the pipelined pass below
+  std::vector<std::pair<std::vector<double>, std::vector<double>>> served;
+  std::vector<SolveReport> blocking;
   for (int k = 0; k < designs; ++k) {
     DensityField d = DensityField::uniform(n, n, cfg.volume_fractions, cfg.density_floor);
     if (k > 0) {
@@ -97,6 +100,8 @@ int main(int argc, char** argv) {
     // the same block through the GPU drop-in
     dev.set_moduli(effective_moduli(d, mat), cfg.solver.omega);
     const SolveReport got = dev.solve(sys.rhs, cfg.solver);
+    served.emplace_back(effective_moduli(d, mat), sys.rhs);
+    blocking.push_back(got);
     const double c_gpu = dev.compliance();
     const auto s_gpu = dev.sensitivities(d, mat);
     double es = 0.0, ef = 0.0;
@@ -126,5 +131,14 @@ int main(int argc, char** argv) {
           ef <= 1e-8 && eoc <= 1e-12))
       ++bad;
   }
-  return bad;
+  // the same designs as one pipelined stream (PcgmgGpu::solve_many): bitwise
+  // the blocking solves
+  const std::vector<SolveReport> many = dev.solve_many(served, cfg.solver, cfg.solver.omega);
+  int diff = 0;
+  for (size_t k = 0; k < many.size(); ++k)
+    if (many[k].solution != blocking[k].solution || many[k].iterations != blocking[k].iterations ||
+        many[k].residual_history != blocking[k].residual_history)
+      ++diff;
+  std::printf("many %zu %d\n", many.size(), diff);
+  return bad + diff;
 }
