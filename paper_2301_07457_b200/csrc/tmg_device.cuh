@@ -41,6 +41,12 @@ constexpr int kStencilPlanes = 19;
 // [x0, x0 + ncol) and stores them as local columns 0 .. ncol-1 with kGX ghost
 // columns on each side (halo of the neighbouring slab, or zeros at the global
 // boundary). A single-GPU level is the slab x0 = 0, ncol = nx + 1.
+// Programmatic dependent launch (griddepcontrol): wait for the prerequisite
+// grid's completion and memory flush (a no-op for a normal launch), and let
+// this grid's dependent launch early.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 struct Grid {
   int nx, ny;  // global elements of the level
   int P;       // padded pitch (nodes)

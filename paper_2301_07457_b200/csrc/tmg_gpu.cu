@@ -432,6 +432,11 @@ struct tmg_gpu_handle {
   // coarse levels up to this many nodes run the V(2,2) halves as shared-memory
   // tiles instead of marching kernels (tmg_stile.cuh)
   long stile_max_nodes = kTileMaxNodes;
+  // tile levels up to these sizes (nodes) take the 2- / 4-coarse-node tiles
+  // instead of the 8-node ones (TMG_STILE_TC2_NODES / TMG_STILE_TC4_NODES)
+  long stile_tc1_nodes = 0, stile_tc2_nodes = kTileTC2Nodes, stile_tc4_nodes = kTileTC4Nodes;
+  // programmatic dependent launch of the V-cycle-bottom kernels (TMG_NO_PDL=1: plain launches)
+  bool pdl = true;
   // two-stage coarse kernels with stage A and stage B on separate warps
   // (tmg_smarch2.cuh; TMG_SMARCH_LOCKSTEP=1 runs the lockstep k_smarch)
   bool smarch_split = true;
@@ -972,10 +977,31 @@ void prolong_level(H* h, Rank& R, int l, const double2* uc, double2* x, bool add
   h->count();
 }
 
+// Launch of a V-cycle-bottom kernel (tile kernels, coarsest solve) with
+// programmatic stream serialization: it starts while its predecessor runs,
+// stages its invariant inputs, and waits (griddepcontrol.wait) before reading
+// what the predecessor writes; each such kernel releases its own dependent
+// only after that wait, so at most one kernel runs ahead. One rank per
+// process only (with per-rank streams the predecessor is an event join).
+template <class... P, class... A>
+void launch_dep(H* h, void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (h->pdl && h->rstreams.empty()) ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...));
+}
+
 void coarse_solve(H* h, Rank& R, const double2* f, double2* u) {
   const int warps = R.n0 / 2, per_block = kCoarseSolveThreads / 32;
-  k_coarse_solve<<<(warps + per_block - 1) / per_block, kCoarseSolveThreads, sizeof(double) * R.n0, h->stream>>>(
-      R.Ainv, R.n0, R.lev[0].g, f, u);
+  launch_dep(h, k_coarse_solve, dim3((warps + per_block - 1) / per_block), dim3(kCoarseSolveThreads),
+             sizeof(double) * R.n0, static_cast<const double*>(R.Ainv), R.n0, R.lev[0].g, f, u);
   CKL();
   h->count();
 }
@@ -1048,9 +1074,17 @@ void launch_smarch(H* h, Rank& R, int l, const double2* x2, const double2* uc, d
   }
   if (!h->dist(l) && static_cast<long>(a.g.nx + 1) * (a.g.ny + 1) <= h->stile_max_nodes) {
     // small level: one shared-memory tile per CTA (tmg_stile.cuh)
-    grid = UP ? dim3((a.g.ny + kTU) / kTU, (a.g.ncol + kTU - 1) / kTU)
-              : dim3((a.gc.ny + kTC) / kTC, (a.gc.ncol + kTC - 1) / kTC);
-    k_stile<UP><<<grid, kTThreads, t_smem<UP>(), h->stream>>>(a);
+    const long nodes = static_cast<long>(a.g.nx + 1) * (a.g.ny + 1);
+    auto tile = [&](auto tc) {
+      constexpr int TC = decltype(tc)::value;
+      const dim3 tg = UP ? dim3((a.g.ny + 2 * TC) / (2 * TC), (a.g.ncol + 2 * TC - 1) / (2 * TC))
+                         : dim3((a.gc.ny + TC) / TC, (a.gc.ncol + TC - 1) / TC);
+      launch_dep(h, k_stile<UP, TC>, tg, dim3(t_threads<TC>()), t_smem<UP, TC>(), a);
+    };
+    if (nodes <= h->stile_tc1_nodes) tile(std::integral_constant<int, 1>{});
+    else if (nodes <= h->stile_tc2_nodes) tile(std::integral_constant<int, 2>{});
+    else if (nodes <= h->stile_tc4_nodes) tile(std::integral_constant<int, 4>{});
+    else tile(std::integral_constant<int, 8>{});
   } else if (h->smarch_split) {
     k_smarch2<UP><<<grid, kS2Threads, sm, h->stream>>>(a);
   } else {
@@ -1864,13 +1898,23 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
                           static_cast<int>(kSSlotDown * s_stages<false>())));
   CK(cudaFuncSetAttribute(k_smarch2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(kSSlotUp * s_stages<true>())));
-  CK(cudaFuncSetAttribute(k_stile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<false>()));
-  CK(cudaFuncSetAttribute(k_stile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<true>()));
+  CK(cudaFuncSetAttribute(k_stile<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<false, 8>()));
+  CK(cudaFuncSetAttribute(k_stile<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<true, 8>()));
+  CK(cudaFuncSetAttribute(k_stile<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<false, 4>()));
+  CK(cudaFuncSetAttribute(k_stile<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<true, 4>()));
+  CK(cudaFuncSetAttribute(k_stile<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<false, 2>()));
+  CK(cudaFuncSetAttribute(k_stile<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<false, 1>()));
+  CK(cudaFuncSetAttribute(k_stile<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<true, 1>()));
+  CK(cudaFuncSetAttribute(k_stile<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<true, 2>()));
   CK(cudaFuncSetAttribute(k_march<StSweep01U, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(StSweep01U::kSlot * kStages)));
   CK(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking));
   if (const char* v = std::getenv("TMG_SMARCH_MIN_NODES")) hp->smarch_min_nodes = std::atol(v);
   if (const char* v = std::getenv("TMG_STILE_MAX_NODES")) hp->stile_max_nodes = std::atol(v);
+  if (const char* v = std::getenv("TMG_NO_PDL")) hp->pdl = std::atoi(v) == 0;
+  if (const char* v = std::getenv("TMG_STILE_TC1_NODES")) hp->stile_tc1_nodes = std::atol(v);
+  if (const char* v = std::getenv("TMG_STILE_TC2_NODES")) hp->stile_tc2_nodes = std::atol(v);
+  if (const char* v = std::getenv("TMG_STILE_TC4_NODES")) hp->stile_tc4_nodes = std::atol(v);
   if (const char* v = std::getenv("TMG_NO_COND_NODES")) hp->cond_nodes = std::atoi(v) == 0;
   if (const char* v = std::getenv("TMG_NO_DEVICE_LOOP")) hp->device_loop = std::atoi(v) == 0;
   if (const char* v = std::getenv("TMG_DENSE_COARSE_FACTOR")) hp->band_factor = std::atoi(v) == 0;

@@ -763,6 +763,8 @@ __global__ void __launch_bounds__(kCoarseSolveThreads) k_coarse_solve(const doub
                                                                       Grid g, const double2* __restrict__ f,
                                                                       double2* __restrict__ u) {
   extern __shared__ double fd[];
+  grid_dep_wait();  // f comes from the restriction just before (tile kernels launch this early)
+  grid_dep_launch();
   const int rows = g.ny + 1, nodes = n / 2;
   for (int k = threadIdx.x; k < nodes; k += blockDim.x) {
     const double2 v = f[g.idx(k / rows, k % rows)];

@@ -10,10 +10,10 @@
 // per-node arithmetic in the same order (s_apply, s_jacobi_r, the
 // restriction sums), so the results are bitwise those of the marching path.
 //
-//   DOWN (coarse block of kTC x kTC nodes, level region 2 kTC + 5 wide):
+//   DOWN (coarse block of TC x TC nodes, level region 2 TC + 5 wide):
 //     x1 = omega f / D; x2 = x1 + omega D^-1 (f - A x1) (written out);
 //     r = f - A x2; f_c = (1/4) P^T r
-//   UP (level block of kTU x kTU nodes, region kTU + 4 wide):
+//   UP (level block of 2 TC x 2 TC nodes, region 2 TC + 4 wide):
 //     w = x2 + P u_c; x3 = w + omega D^-1 (f - A w);
 //     x4 = x3 + omega D^-1 (f - A x3) (written out)
 #pragma once
@@ -25,45 +25,55 @@
 
 namespace tmg {
 
-constexpr int kTC = 8;                 // DOWN: coarse nodes per CTA side
-constexpr int kTDW = 2 * kTC + 5;      // DOWN region side (level nodes 2X0-3 .. 2X0+2kTC+1)
-constexpr int kTU = 16;                // UP: level nodes per CTA side
-constexpr int kTUW = kTU + 4;          // UP region side (x0-2 .. x0+kTU+1)
-constexpr int kTUC = kTU / 2 + 4;      // UP coarse region side
-constexpr int kTThreads = 512;
+// Tile sizes: DOWN covers TC x TC coarse nodes per CTA, UP 2 TC x 2 TC level
+// nodes. The stages of a tile are issue-bound on one SM (a %globaltimer trace
+// of the 8-node tiles: ~1 us per stage for a 441-node region), so the small
+// levels take small tiles spread over more SMs: the halo redundancy costs
+// nothing there, the per-SM node count sets the stage time.
+template <int TC>
+__host__ __device__ constexpr int t_threads() { return TC >= 8 ? 512 : (TC >= 4 ? 256 : (TC >= 2 ? 128 : 64)); }
+template <bool UP, int TC>
+__host__ __device__ constexpr int t_side() { return UP ? 2 * TC + 4 : 2 * TC + 5; }
+template <bool UP, int TC>
+__host__ __device__ constexpr int t_nodes() { return t_side<UP, TC>() * t_side<UP, TC>(); }
+template <int TC>
+__host__ __device__ constexpr int t_uc_side() { return TC + 4; }  // UP coarse region side
 // default size limit of a tile-kernel level (nodes); TMG_STILE_MAX_NODES overrides
 constexpr long kTileMaxNodes = 257L * 257L;
+// default tile sizes by level size (measured, c0/c1/c2/c3): 2-node tiles up to
+// 65^2 nodes, 4-node tiles up to 129^2, 8-node tiles above
+constexpr long kTileTC2Nodes = 65L * 65L, kTileTC4Nodes = 129L * 129L;
 
-template <bool UP>
-__host__ __device__ constexpr int t_side() { return UP ? kTUW : kTDW; }
-template <bool UP>
-__host__ __device__ constexpr int t_nodes() { return t_side<UP>() * t_side<UP>(); }
-// shared memory: planes, f, two stage buffers, then (DOWN) the residual block
+// shared memory: planes, f, the reciprocal diagonal, two stage buffers, then
+// (DOWN) the residual block
 // or (UP) x2 and the coarse correction
 // planes region in doubles, padded to 16 bytes for the double2 buffers after it
-template <bool UP>
-__host__ __device__ constexpr int t_plane_doubles() { return (kStencilPlanes * t_nodes<UP>() + 1) & ~1; }
-template <bool UP>
+template <bool UP, int TC>
+__host__ __device__ constexpr int t_plane_doubles() { return (kStencilPlanes * t_nodes<UP, TC>() + 1) & ~1; }
+template <bool UP, int TC>
 __host__ __device__ constexpr int t_smem() {
-  return t_plane_doubles<UP>() * 8 + t_nodes<UP>() * 3 * 16 +
-         (UP ? t_nodes<true>() * 16 + kTUC * kTUC * 16 : (2 * kTC + 1) * (2 * kTC + 1) * 16);
+  return t_plane_doubles<UP, TC>() * 8 + t_nodes<UP, TC>() * 4 * 16 +
+         (UP ? t_nodes<true, TC>() * 16 + t_uc_side<TC>() * t_uc_side<TC>() * 16 : (2 * TC + 1) * (2 * TC + 1) * 16);
 }
 
 // plane k of the region column whose row 0 is `col` (plane stride = region nodes)
-template <bool UP>
+template <int N>
 struct TPlanes {
   const double* col;
-  __device__ __forceinline__ double at(int k, int j) const { return col[k * t_nodes<UP>() + j]; }
+  __device__ __forceinline__ double at(int k, int j) const { return col[k * N + j]; }
 };
 
-template <bool UP>
-__global__ void __launch_bounds__(kTThreads) k_stile(const __grid_constant__ SMarchArgs a) {
+template <bool UP, int TC>
+__global__ void __launch_bounds__(t_threads<TC>()) k_stile(const __grid_constant__ SMarchArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  constexpr int W = t_side<UP>();
-  constexpr int N = t_nodes<UP>();
+  constexpr int W = t_side<UP, TC>();
+  constexpr int N = t_nodes<UP, TC>();
+  constexpr int kTThreads = t_threads<TC>();
+  constexpr int kTU = 2 * TC, kTUC = t_uc_side<TC>(), kTC = TC;
   double* pl = reinterpret_cast<double*>(smem_raw);       // [19][W][W]
-  double2* fv = reinterpret_cast<double2*>(pl + t_plane_doubles<UP>());
-  double2* sa = fv + N;  // stage-A inputs (x1 / w)
+  double2* fv = reinterpret_cast<double2*>(pl + t_plane_doubles<UP, TC>());
+  double2* rcv = fv + N;  // 1/D of the region (rcp_nr of planes 0 and 2), formed once
+  double2* sa = rcv + N;  // stage-A inputs (x1 / w)
   double2* sb = sa + N;  // stage-A outputs (x2 / x3)
   double2* ex = sb + N;  // DOWN: residual block; UP: x2 over the region, then u_c
   const Grid& g = a.g;
@@ -73,16 +83,31 @@ __global__ void __launch_bounds__(kTThreads) k_stile(const __grid_constant__ SMa
   const int oy = UP ? blockIdx.x * kTU - 2 : 2 * blockIdx.x * kTC - 3;
   auto in_level = [&](int x, int y) { return g.x0 + x >= 0 && g.x0 + x <= g.nx && y >= 0 && y <= g.ny; };
   const double2 z2 = make_double2(0.0, 0.0);
-  // ---- load the region (zeros outside the level, where every array is zero)
+  // ---- load the region (zeros outside the level, where every array is
+  // zero). Before griddepcontrol.wait only data no kernel of the solve writes
+  // (the stencil planes, from setup) or that the kernel two launches back
+  // finished (UP: f and x2, from this level's DOWN half): a launch with
+  // programmatic stream serialization starts while its predecessor runs, and
+  // every tile kernel lets its dependent launch only after its own wait.
   for (int n = t; n < N; n += kTThreads) {
     const int x = ox + n / W, y = oy + n % W;
     const bool in = in_level(x, y);
     const long i = in ? g.idx(x, y) : 0;
+    double p[kStencilPlanes];
 #pragma unroll
-    for (int k = 0; k < kStencilPlanes; ++k) pl[k * N + n] = in ? a.S[k * g.size + i] : 0.0;
-    fv[n] = in ? a.f[i] : z2;
-    if (UP) ex[n] = in ? a.x2[i] : z2;
+    for (int k = 0; k < kStencilPlanes; ++k) p[k] = in ? a.S[k * g.size + i] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kStencilPlanes; ++k) pl[k * N + n] = p[k];
+    // the reciprocal diagonal (rcp_nr of planes 0 and 2, the d of s_apply),
+    // formed once for the DOWN stage-A input and stage A, UP stages A and B
+    rcv[n] = make_double2(rcp_nr(p[0]), rcp_nr(p[2]));
+    if (UP) {
+      fv[n] = in ? a.f[i] : z2;
+      ex[n] = in ? a.x2[i] : z2;
+    }
   }
+  grid_dep_wait();
+  grid_dep_launch();
   double2* uc = ex + N;  // UP: coarse region kTUC x kTUC from coarse node (cx0, cy0)
   const int cx0 = (ox >> 1) - 1, cy0 = (oy >> 1) - 1;  // ox, oy even for UP
   if (UP) {
@@ -91,9 +116,14 @@ __global__ void __launch_bounds__(kTThreads) k_stile(const __grid_constant__ SMa
       const bool in = a.gc.x0 + X >= 0 && a.gc.x0 + X <= a.gc.nx && Y >= 0 && Y <= a.gc.ny;
       uc[n] = in ? a.uc[a.gc.idx(X, Y)] : z2;
     }
+  } else {
+    for (int n = t; n < N; n += kTThreads) {
+      const int x = ox + n / W, y = oy + n % W;
+      fv[n] = in_level(x, y) ? a.f[g.idx(x, y)] : z2;
+    }
   }
   __syncthreads();
-  auto D = [&](int n) { return make_double2(rcp_nr(pl[n]), rcp_nr(pl[2 * N + n])); };
+  auto D = [&](int n) { return rcv[n]; };
   // y = A v at local (i, j) over the buffer v, its diagonal in d
   auto apply = [&](const double2* v, int i, int j, double2& y, double2& d) {
     double2 l[3], c[3], r[3];
@@ -103,7 +133,7 @@ __global__ void __launch_bounds__(kTThreads) k_stile(const __grid_constant__ SMa
       c[q] = v[i * W + j - 1 + q];
       r[q] = v[(i + 1) * W + j - 1 + q];
     }
-    s_apply(TPlanes<UP>{pl + i * W}, TPlanes<UP>{pl + (i - 1) * W}, j, l, c, r, y, d);
+    s_apply(TPlanes<N>{pl + i * W}, TPlanes<N>{pl + (i - 1) * W}, j, l, c, r, y, d);
   };
   // ---- stage-A inputs over the whole region
   for (int n = t; n < N; n += kTThreads) {
@@ -139,7 +169,7 @@ __global__ void __launch_bounds__(kTThreads) k_stile(const __grid_constant__ SMa
     const int m = i * W + j;
     double2 yv, d;
     apply(sa, i, j, yv, d);
-    const double2 rc = UP ? make_double2(rcp_nr(d.x), rcp_nr(d.y)) : D(m);
+    const double2 rc = D(m);  // = rcp_nr of d = (c00, c11), planes 0 and 2
     const double2 v = in_level(x, y) ? s_jacobi_r(sa[m], fv[m], yv, rc, a.omega) : z2;
     sb[m] = v;
     // DOWN: x2 of the level nodes this CTA owns (level block [2X0, 2X0+2kTC))
@@ -155,7 +185,7 @@ __global__ void __launch_bounds__(kTThreads) k_stile(const __grid_constant__ SMa
     apply(sb, i, j, yv, d);
     const bool ok = in_level(x, y);
     if (UP) {
-      const double2 v = ok ? s_jacobi_r(sb[m], fv[m], yv, make_double2(rcp_nr(d.x), rcp_nr(d.y)), a.omega) : z2;
+      const double2 v = ok ? s_jacobi_r(sb[m], fv[m], yv, D(m), a.omega) : z2;
       if (x < g.ncol && y <= g.ny && x >= 0) a.out[g.idx(x, y)] = v;
     } else {
       ex[(i - 2) * (W - 4) + (j - 2)] = ok ? make_double2(fv[m].x - yv.x, fv[m].y - yv.y) : z2;

@@ -447,6 +447,38 @@ def test_tile_kernels_match_marching(monkeypatch, nx, ny, nc, recipe, gamma):
 
 
 @pytest.mark.parametrize("nx,ny,nc,recipe,gamma", [(64, 64, 3, "iid", 1), (256, 128, 5, "checker", 1),
+                                                   (96, 160, 4, "iid", 2), (512, 512, 6, "iid", 1)])
+def test_tile_sizes_and_dependent_launch_are_bitwise(monkeypatch, nx, ny, nc, recipe, gamma):
+    """The tile kernels come in 1/2/4/8-node sizes (TMG_STILE_TC{1,2,4}_NODES)
+    and the V-cycle bottom launches with programmatic stream serialization
+    (TMG_NO_PDL=1 turns it off); every combination performs the same per-node
+    arithmetic, so solves, histories and one cycle are bitwise equal."""
+    _, E = moduli(nx, ny, recipe, 8)
+    g = P.GridLevel(nx, ny)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    b = P.assemble_rhs(g, bc)
+    cfg = P.SolverConfig(tol=1e-10, max_iter=500, gamma=gamma)
+    f = np.random.default_rng(9).standard_normal(b.size)
+    reps = []
+    for env in ({}, {"TMG_NO_PDL": "1", "TMG_STILE_TC2_NODES": "0", "TMG_STILE_TC4_NODES": "0"},
+                {"TMG_STILE_TC1_NODES": "1000000"}, {"TMG_STILE_TC4_NODES": "1000000", "TMG_STILE_TC2_NODES": "0"}):
+        for k in ("TMG_NO_PDL", "TMG_STILE_TC1_NODES", "TMG_STILE_TC2_NODES", "TMG_STILE_TC4_NODES"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        ops = P.MultigridOperators(g, nc, 0.3, bc)
+        ops.set_moduli(E, 0.6)
+        rep = P.pcgmg_solve(ops, b, cfg)
+        reps.append((rep, P.compliance(ops), P.mg_cycle(ops, np.zeros_like(f), f, gamma=gamma)))
+    a, ca, va = reps[0]
+    assert a.converged
+    for c, cc, vc in reps[1:]:
+        assert a.iterations == c.iterations and a.residual_history == c.residual_history
+        assert np.array_equal(a.solution, c.solution) and ca == cc
+        assert np.array_equal(va, vc)
+
+
+@pytest.mark.parametrize("nx,ny,nc,recipe,gamma", [(64, 64, 3, "iid", 1), (256, 128, 5, "checker", 1),
                                                    (96, 160, 4, "iid", 2), (1024, 512, 7, "iid", 1)])
 def test_specialised_coarse_kernels_are_bitwise(monkeypatch, nx, ny, nc, recipe, gamma):
     """The two-stage coarse kernels with stage A and stage B on separate warps
