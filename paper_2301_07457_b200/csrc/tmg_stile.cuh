@@ -84,30 +84,40 @@ __global__ void __launch_bounds__(t_threads<TC>()) k_stile(const __grid_constant
   auto in_level = [&](int x, int y) { return g.x0 + x >= 0 && g.x0 + x <= g.nx && y >= 0 && y <= g.ny; };
   const double2 z2 = make_double2(0.0, 0.0);
   // ---- load the region (zeros outside the level, where every array is
-  // zero). Before griddepcontrol.wait only data no kernel of the solve writes
-  // (the stencil planes, from setup) or that the kernel two launches back
-  // finished (UP: f and x2, from this level's DOWN half): a launch with
-  // programmatic stream serialization starts while its predecessor runs, and
-  // every tile kernel lets its dependent launch only after its own wait.
-  for (int n = t; n < N; n += kTThreads) {
-    const int x = ox + n / W, y = oy + n % W;
-    const bool in = in_level(x, y);
-    const long i = in ? g.idx(x, y) : 0;
-    double p[kStencilPlanes];
+  // zero), one node per thread. A launch with programmatic stream
+  // serialization starts while its predecessor still runs; until
+  // griddepcontrol.wait it only issues loads, into registers, of data no
+  // kernel of the solve writes (the stencil planes, from setup) or that the
+  // kernel two launches back finished (UP: f and x2, from this level's DOWN
+  // half; every tile kernel lets its dependent launch only after its own
+  // wait). Nothing is stored before the wait: shared-memory contents written
+  // there were found corrupted, non-deterministically, when the CTA shared an
+  // SM with the predecessor's k_smarch2 CTAs.
+  static_assert(N <= kTThreads, "one region node per thread");
+  const int n0 = t;
+  const bool own = n0 < N;
+  const int x0n = ox + n0 / W, y0n = oy + n0 % W;
+  const bool in0 = own && in_level(x0n, y0n);
+  const long i0 = in0 ? g.idx(x0n, y0n) : 0;
+  double p[kStencilPlanes];
 #pragma unroll
-    for (int k = 0; k < kStencilPlanes; ++k) p[k] = in ? a.S[k * g.size + i] : 0.0;
-#pragma unroll
-    for (int k = 0; k < kStencilPlanes; ++k) pl[k * N + n] = p[k];
-    // the reciprocal diagonal (rcp_nr of planes 0 and 2, the d of s_apply),
-    // formed once for the DOWN stage-A input and stage A, UP stages A and B
-    rcv[n] = make_double2(rcp_nr(p[0]), rcp_nr(p[2]));
-    if (UP) {
-      fv[n] = in ? a.f[i] : z2;
-      ex[n] = in ? a.x2[i] : z2;
-    }
+  for (int k = 0; k < kStencilPlanes; ++k) p[k] = in0 ? a.S[k * g.size + i0] : 0.0;
+  double2 f0 = z2, x20 = z2;
+  if (UP && in0) {
+    f0 = a.f[i0];
+    x20 = a.x2[i0];
   }
   grid_dep_wait();
   grid_dep_launch();
+  if (own) {
+#pragma unroll
+    for (int k = 0; k < kStencilPlanes; ++k) pl[k * N + n0] = p[k];
+    // the reciprocal diagonal (rcp_nr of planes 0 and 2, the d of s_apply),
+    // formed once for the DOWN stage-A input and stage A, UP stages A and B
+    rcv[n0] = make_double2(rcp_nr(p[0]), rcp_nr(p[2]));
+    fv[n0] = UP ? f0 : (in0 ? a.f[i0] : z2);
+    if (UP) ex[n0] = x20;
+  }
   double2* uc = ex + N;  // UP: coarse region kTUC x kTUC from coarse node (cx0, cy0)
   const int cx0 = (ox >> 1) - 1, cy0 = (oy >> 1) - 1;  // ox, oy even for UP
   if (UP) {
@@ -115,11 +125,6 @@ __global__ void __launch_bounds__(t_threads<TC>()) k_stile(const __grid_constant
       const int X = cx0 + n / kTUC, Y = cy0 + n % kTUC;
       const bool in = a.gc.x0 + X >= 0 && a.gc.x0 + X <= a.gc.nx && Y >= 0 && Y <= a.gc.ny;
       uc[n] = in ? a.uc[a.gc.idx(X, Y)] : z2;
-    }
-  } else {
-    for (int n = t; n < N; n += kTThreads) {
-      const int x = ox + n / W, y = oy + n % W;
-      fv[n] = in_level(x, y) ? a.f[g.idx(x, y)] : z2;
     }
   }
   __syncthreads();
