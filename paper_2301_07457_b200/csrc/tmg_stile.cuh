@@ -90,9 +90,8 @@ __global__ void __launch_bounds__(t_threads<TC>()) k_stile(const __grid_constant
   // kernel of the solve writes (the stencil planes, from setup) or that the
   // kernel two launches back finished (UP: f and x2, from this level's DOWN
   // half; every tile kernel lets its dependent launch only after its own
-  // wait). Nothing is stored before the wait: shared-memory contents written
-  // there were found corrupted, non-deterministically, when the CTA shared an
-  // SM with the predecessor's k_smarch2 CTAs.
+  // wait). Nothing is stored before the wait (the conservative form; see the
+  // dependent-launch race in DESIGN.md section 4).
   static_assert(N <= kTThreads, "one region node per thread");
   const int n0 = t;
   const bool own = n0 < N;
