@@ -871,7 +871,7 @@ Grid coarse_of(H* h, Rank& R, int l, long& off) {
 template <class Stage, bool RED>
 void launch_march(H* h, MarchArgs a) {
   dim3 grid;
-  const size_t sm = static_cast<size_t>(Stage::kSlot) * kStages;
+  const size_t sm = static_cast<size_t>(Stage::kSlot) * RingOf<Stage>::value;
   if constexpr (Stage::kRow0 == -1) {  // restriction: tiles of coarse rows / columns
     const long ty = (a.gc.ny + 1 + Stage::kOwned / 2 - 1) / (Stage::kOwned / 2);
     a.tx = strip_tx(ty, a.gc.ncol, 2);
@@ -1907,7 +1907,7 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
   CK(cudaFuncSetAttribute(k_stile<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<true, 1>()));
   CK(cudaFuncSetAttribute(k_stile<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem<true, 2>()));
   CK(cudaFuncSetAttribute(k_march<StSweep01U, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          static_cast<int>(StSweep01U::kSlot * kStages)));
+                          static_cast<int>(StSweep01U::kSlot * RingOf<StSweep01U>::value)));
   CK(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking));
   if (const char* v = std::getenv("TMG_SMARCH_MIN_NODES")) hp->smarch_min_nodes = std::atol(v);
   if (const char* v = std::getenv("TMG_STILE_MAX_NODES")) hp->stile_max_nodes = std::atol(v);

@@ -46,6 +46,14 @@ constexpr int kTY = 128;                 // consumer threads (rows) per CTA
 constexpr int kConsumerWarps = kTY / 32;
 constexpr int kMarchThreads = kTY + 32;  // + one producer warp
 constexpr int kStages = 6;
+// ring depth of the fused PCG-update pass (StSweep01U): its slots carry six
+// streams, so six stages left room for three CTAs per SM; four stages give
+// the register limit's four (same-box A/B, TMG_UPD_STAGES builds: c4 6.37 ->
+// 6.21 ms per PCG iteration, c3 0.230 -> 0.224 ms, c1 unchanged; 5 stages in
+// between)
+#ifndef TMG_UPD_STAGES
+#define TMG_UPD_STAGES 4
+#endif
 constexpr long kSlackNodes = 1024;  // every field is over-allocated by this
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -397,6 +405,7 @@ struct StResidual : WithF<0> {
 template <bool UPD>
 struct StSweep01T {
   static constexpr int NS = UPD ? 6 : 3, kRow0 = 0, kOwned = kTY, kLead = 1;
+  static constexpr int kRing = UPD ? TMG_UPD_STAGES : kStages;
   static constexpr int O_F = 0, O_E = O_F + sbytes(kTY + 2, 16), O_M = O_E + sbytes(kTY + 4, 8);
   static constexpr int O_A = O_M + sbytes(kTY + 2, 1);  // UPD: A p_old, window rows
   static constexpr int O_X = O_A + sbytes(kTY + 2, 16);  // UPD: x, own rows
@@ -658,6 +667,16 @@ struct CarryOf<Stage, std::void_t<typename Stage::Carry>> {
   static constexpr bool used = true;
 };
 
+// Ring depth of a stage: Stage::kRing where declared, else kStages
+template <class Stage, class = void>
+struct RingOf {
+  static constexpr int value = kStages;
+};
+template <class Stage>
+struct RingOf<Stage, std::void_t<decltype(Stage::kRing)>> {
+  static constexpr int value = Stage::kRing;
+};
+
 // Column range of one CTA: ring entries [cf, cl]; run() is called for every
 // window centre x in [xlo, xhi] (restriction stage: every fine column it
 // marches; others: the owned node columns).
@@ -681,6 +700,7 @@ __device__ __forceinline__ void march_range(const MarchArgs& a, int& cf, int& cl
 template <class Stage, bool RED>
 __global__ void __launch_bounds__(kMarchThreads) k_march(MarchArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  constexpr int kStages = RingOf<Stage>::value;
   __shared__ uint64_t full[kStages], empty[kStages];
 
   const Grid& g = a.g;
