@@ -981,8 +981,9 @@ void prolong_level(H* h, Rank& R, int l, const double2* uc, double2* x, bool add
 // programmatic stream serialization: it starts while its predecessor runs,
 // stages its invariant inputs, and waits (griddepcontrol.wait) before reading
 // what the predecessor writes; each such kernel releases its own dependent
-// only after that wait, so at most one kernel runs ahead. One rank per
-// process only (with per-rank streams the predecessor is an event join).
+// only after that wait, so at most one kernel runs ahead. Single-rank
+// handles only: slab handles interleave event joins (LocalComm) or NCCL
+// collectives (multi-rank NCCL never ran here) with the bottom kernels.
 template <class... P, class... A>
 void launch_dep(H* h, void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, A&&... args) {
   cudaLaunchConfig_t cfg{};
@@ -994,7 +995,7 @@ void launch_dep(H* h, void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, 
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = (h->pdl && h->rstreams.empty()) ? 1 : 0;
+  cfg.numAttrs = (h->pdl && !h->distributed) ? 1 : 0;
   CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...));
 }
 
