@@ -1,12 +1,16 @@
-# Round-2 final measurement set (after the small-tile and dependent-launch V-cycle bottom)
-# solve config with clock samples (small configs with enough steps for the
-# 100 ms nvidia-smi sampler), the reference arm with the driver's step counts,
-# the optimizer / OC / Poisson benches, the ncu launch list of a short bench
-# run and `ncu --set full` of one c4 PCG iteration's fine and coarse passes.
-# ncu runs use TMG_NO_COND_NODES=1 (ncu cannot profile kernels inside graphs
-# with conditional nodes; the kernels are identical).
+# Round-2 final measurement set (under gpurun, repo root), after the small
+# tiles, the dependent-launch V-cycle bottom and the four-stage PCG-update
+# ring: the GPU test suite and smoke(), bench lines of every solve config with
+# clock samples (small configs with enough steps for the 100 ms nvidia-smi
+# sampler), the reference arm with the driver's step counts, the optimizer
+# bench, the ncu launch list of a short bench run, `ncu --set full` of one c4
+# PCG iteration's fine and coarse passes, and warm-cache launch lists of c1
+# and c3. ncu runs use TMG_NO_COND_NODES=1 (ncu cannot profile kernels inside
+# graphs with conditional nodes; the kernels are identical).
 set -x
 o=gpurun_out/r02c; mkdir -p $o
+timeout 1500 python -m pytest tests -m gpu -q > $o/gputest.log 2>&1; echo gputest=$?
+python -c "import __graft_entry__ as g; g.smoke()" > $o/smoke.log 2>&1; echo smoke=$?
 python bench.py --steps 20 --warmup 5 > $o/bench_c4.json 2> $o/bench_c4.err; echo bench=$?
 python bench.py --impl reference --steps 20 --warmup 5 > $o/bench_ref.json 2> $o/bench_ref.err; echo ref=$?
 python bench.py --config c1 --steps 400 --warmup 20 --no-cpu-baseline > $o/bench_c1.json 2>&1; echo c1=$?
