@@ -60,3 +60,27 @@ def test_nccl_one_rank_conditional_graphs(monkeypatch):
     for cfg in (P.SolverConfig(tol=1e-8, max_iter=1000, num_coarsenings=5),
                 P.SolverConfig(tol=1e-12, max_iter=7, num_coarsenings=5)):
         _same(P.pcgmg_solve(one, b, cfg), P.pcgmg_solve(nccl, b, cfg))
+
+
+def test_nccl_one_rank_pipelined_solves_are_bitwise_the_single_rank_ones():
+    """The bench's e2e leg at N > 1 runs the pipelined calls
+    (tmg_gpu_stage_inputs / tmg_gpu_solve_staged / tmg_gpu_sync_outputs) on an
+    NCCL handle: staged uploads of the rank's slab, the install, the setup with
+    its plane gathers and the solve must give, problem for problem, bitwise
+    the blocking single-rank solves."""
+    g = P.GridLevel(256, 256)
+    bc = P.wall_boundary_conditions(g, "uniform")
+    cfg = P.SolverConfig(tol=1e-9, max_iter=2000)
+    probs = []
+    for k in range(3):
+        _, E = moduli(256, 256, "iid" if k % 2 == 0 else "checker", 30 + k)
+        probs.append((E, P.assemble_rhs(g, bc)))
+    one = P.MultigridOperators(g, 5, 0.3, bc)
+    want = []
+    for E, b in probs:
+        one.set_moduli(E, 0.6)
+        want.append(P.pcgmg_solve(one, b, cfg))
+    nccl = P.MultigridOperators(g, 5, 0.3, bc, nccl=(1, 0, P.nccl_unique_id()))
+    got = P.pcgmg_solve_many(nccl, probs, cfg, 0.6)
+    for r, w in zip(got, want):
+        _same(r, w)
