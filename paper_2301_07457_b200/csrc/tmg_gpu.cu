@@ -504,6 +504,19 @@ int pow2_strip(long rows_tiles, long cols, int a) {
       best = tx;
     }
   }
+  // A grid that still takes two or more waves but would fit the device in
+  // one at twice the strip width (four resident CTAs per SM, the fine passes'
+  // measured occupancy) takes the single wave: its second wave's ring fill and
+  // launch cost more than the longer strips on L2-resident meshes (c3 mesh
+  // 1024^2: 8 -> 16 columns, -3 % per PCG iteration). Wider single-wave
+  // strips (c2: 16 -> 64) measured slower. TMG_STRIP_ONE_WAVE=0 turns it off.
+  static const bool one_wave = [] {
+    const char* e = std::getenv("TMG_STRIP_ONE_WAVE");
+    return !e || std::atoi(e) != 0;
+  }();
+  const long ctas = rows_tiles * ((cols + best - 1) / best);
+  const long ctas2 = rows_tiles * ((cols + 2 * best - 1) / (2 * best));
+  if (one_wave && best < 64 && ctas > 4L * 148 && ctas2 <= 4L * 148) best *= 2;
   return best;
 }
 
