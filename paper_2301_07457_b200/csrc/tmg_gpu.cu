@@ -227,6 +227,18 @@ struct Comm {
   virtual void gather_columns(std::vector<Rank*>& rs, int level, const std::function<void*(Rank&)>& field,
                               size_t esize, long plane_stride, int planes, const std::vector<int>& X0,
                               const std::vector<int>& ncol, cudaStream_t s) = 0;
+  // several ghost exchanges at one point of the schedule (same fields and
+  // widths as the separate calls, in this order): NCCL issues them as one
+  // group, one launch and one latency instead of one per field
+  struct HaloReq {
+    int level;
+    std::function<void*(Rank&)> field;
+    size_t esize;
+    int wl, wr;
+  };
+  virtual void halo_many(std::vector<Rank*>& rs, const std::vector<HaloReq>& reqs, cudaStream_t s) {
+    for (const HaloReq& q : reqs) halo(rs, q.level, q.field, q.esize, q.wl, q.wr, s);
+  }
   // partials[0 .. n) of every rank summed elementwise into gparts of every
   // rank (each element has one non-zero contributor, so the sum is exact)
   virtual void allreduce(std::vector<Rank*>& rs, int n, cudaStream_t s) = 0;
@@ -312,11 +324,24 @@ struct NcclComm : Comm {
   bool local() const override { return false; }
   void halo(std::vector<Rank*>& rs, int level, const std::function<void*(Rank&)>& field, size_t esize, int wl,
             int wr, cudaStream_t s) override {
+    NK(nccl().groupStart());
+    halo_ops(rs, level, field, esize, wl, wr, s);
+    NK(nccl().groupEnd());
+  }
+  void halo_many(std::vector<Rank*>& rs, const std::vector<HaloReq>& reqs, cudaStream_t s) override {
+    NK(nccl().groupStart());
+    for (const HaloReq& q : reqs) halo_ops(rs, q.level, q.field, q.esize, q.wl, q.wr, s);
+    NK(nccl().groupEnd());
+  }
+  // the sends and receives of one exchange (inside a group); both sides issue
+  // them in the same order, which is how NCCL pairs several messages between
+  // the same two ranks within a group
+  void halo_ops(std::vector<Rank*>& rs, int level, const std::function<void*(Rank&)>& field, size_t esize, int wl,
+                int wr, cudaStream_t s) {
     Rank& me = *rs[0];
     const Grid& g = me.lev[level].g;
     const size_t col = esize * g.P;
     char* mine = static_cast<char*>(field(me));
-    NK(nccl().groupStart());
     if (rank > 0) {
       // my first wr columns to the left neighbour's right ghost; its last wl to my left ghost
       if (wr > 0) NK(nccl().send(mine + kGX * col, wr * col, ncclChar, rank - 1, comm, s));
@@ -326,7 +351,6 @@ struct NcclComm : Comm {
       if (wl > 0) NK(nccl().send(mine + (g.ncol + kGX - wl) * col, wl * col, ncclChar, rank + 1, comm, s));
       if (wr > 0) NK(nccl().recv(mine + (kGX + g.ncol) * col, wr * col, ncclChar, rank + 1, comm, s));
     }
-    NK(nccl().groupEnd());
   }
   void gather_columns(std::vector<Rank*>& rs, int level, const std::function<void*(Rank&)>& field, size_t esize,
                       long plane_stride, int planes, const std::vector<int>& X0, const std::vector<int>& ncol,
@@ -749,6 +773,22 @@ void alloc_rank(H* h, Rank& R) {
 void halo_vec(H* h, int l, const std::function<double2*(Rank&)>& field, int wl = 1, int wr = 1) {
   if (!h->dist(l)) return;
   h->comm->halo(h->ranks, l, [&](Rank& R) -> void* { return field(R); }, sizeof(double2), wl, wr, h->stream);
+}
+// several vector exchanges at one point (level, field, wl, wr each): one
+// NCCL group; levels that are not distributed are skipped
+struct VecHalo {
+  int level;
+  std::function<double2*(Rank&)> field;
+  int wl, wr;
+};
+void halo_vecs(H* h, const std::vector<VecHalo>& hs) {
+  std::vector<Comm::HaloReq> reqs;
+  for (const VecHalo& v : hs) {
+    if (!h->dist(v.level)) continue;
+    auto f = v.field;
+    reqs.push_back({v.level, [f](Rank& R) -> void* { return f(R); }, sizeof(double2), v.wl, v.wr});
+  }
+  if (!reqs.empty()) h->comm->halo_many(h->ranks, reqs, h->stream);
 }
 
 // replicated level l: every rank's owned columns to all ranks
@@ -1215,16 +1255,16 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
   auto ccur = [&](Rank& R) { return R.lev[l - 1].u[R.lev[l - 1].cur]; };
   // the two-stage UP pass prolongates onto two ghost columns on the right:
   // column ncol+1 interpolates coarse columns ncol/2 and ncol/2 + 1
-  if (cdist) halo_vec(h, l - 1, ccur, 1, 2);
   int p = 0;
   if (!fine && big && !zero && post == 2) {
-    // coarse level: prolongation + both post-sweeps in one pass
-    halo_vec(h, l, cur, 2, 2);
-    halo_vec(h, l, [&](Rank& R) { return R.lev[l].f; }, 3, 2);
+    // coarse level: prolongation + both post-sweeps in one pass; its three
+    // inputs' ghosts (coarse correction, iterate, rhs) in one exchange
+    halo_vecs(h, {{l - 1, ccur, 1, 2}, {l, cur, 2, 2}, {l, [&](Rank& R) { return R.lev[l].f; }, 3, 2}});
     for_ranks(h, [&](Rank& R) { launch_smarch<true>(h, R, l, cur(R), ccur(R), nxt(R), nullptr); });
     flip();
     p = post;
   } else if (fine && !zero && post >= 1) {
+    if (cdist) halo_vec(h, l - 1, ccur, 1, 2);
     for_ranks(h, [&](Rank& Rk) {
       Rank* R = &Rk;
       MarchArgs a = march_args(h, *R, cur(*R));
@@ -1238,6 +1278,7 @@ bool enqueue_cycle(H* h, int l, bool zero, int gamma, int pre, int post, RedOp z
     flip();
     p = 1;
   } else {
+    if (cdist) halo_vec(h, l - 1, ccur, 1, 2);
     for_ranks(h, [&](Rank& R) { prolong_level(h, R, l, ccur(R), cur(R), !zero); });
   }
   bool fused = false;
@@ -1319,12 +1360,13 @@ void enqueue_iteration(H* h, int k, bool first, bool fused_upd, int gamma, int p
     a.red_out = out;
     launch_march<StPupd, true>(h, a);
   });
-  halo_vec(h, nc, [&](Rank& R) { return R.pbuf[k ^ 1]; });
   if (fused_upd) {
     // x and r are updated by the next iteration's first pass (or by
-    // finish_update after the last one); it reads A p with halo
-    halo_vec(h, nc, [&](Rank& R) { return R.ap; });
+    // finish_update after the last one); it reads A p with halo (p and A p
+    // in one exchange)
+    halo_vecs(h, {{nc, [&](Rank& R) { return R.pbuf[k ^ 1]; }, 1, 1}, {nc, [&](Rank& R) { return R.ap; }, 1, 1}});
   } else {
+    halo_vec(h, nc, [&](Rank& R) { return R.pbuf[k ^ 1]; });
     // x += alpha p; r -= alpha Ap; rr (solvers.cpp:383-386)
     reduce(h, kRedRr, [&](Rank& R, RedOp rop, double* out) {
       const Grid& g = R.fine().g;
