@@ -1651,7 +1651,7 @@ void setup(H* h, double omega) {
     const size_t bsm = static_cast<size_t>(n) * (b + 2) * sizeof(double);
     if (h->band_factor && b <= 31 && bsm <= 200 * 1024) {
       CK(cudaFuncSetAttribute(k_cholesky_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bsm)));
-      k_cholesky_band<<<1, 32, bsm, h->stream>>>(R->A0, n, b, R->bad_row);
+      k_cholesky_band<<<1, kCholBandThreads, bsm, h->stream>>>(R->A0, n, b, R->bad_row);
     } else {
       launch_cholesky(h->stream, R->A0, n, R->bad_row);
     }

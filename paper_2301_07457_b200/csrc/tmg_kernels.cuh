@@ -613,53 +613,77 @@ __global__ void __launch_bounds__(1024) k_cholesky(double* __restrict__ Ag, int 
   if (t == 0) *bad_row = fail;
 }
 
-// Banded Cholesky of the coarsest matrix in one warp. With the column-major
+// Banded Cholesky of the coarsest matrix in one CTA. With the column-major
 // node numbering the 9-point coarsest operator has lower half-bandwidth
 // b = 2 (ny + 2) + 1 dofs, and its factor has no fill outside the band (the
 // envelope the reference's CholeskyFactor exploits, solvers.cpp:89-148), so
-// only the band is staged in shared memory (Bs[i][d] = A[i][i-d]). Lane r
-// owns row k+1+r of step k and takes the other lanes' multipliers by
-// shuffles. Inside the band every entry sees the same operations in the same
-// order as in k_cholesky (outside it both leave exact zeros), so the factor
-// and the failing row are bitwise those of the dense kernel. b <= 31.
-__global__ void __launch_bounds__(32) k_cholesky_band(double* __restrict__ Ag, int n, int b, int* bad_row) {
+// only the band is staged in shared memory (Bs[i][d] = A[i][i-d]). Step k:
+// b threads form the multipliers l_{k+1..k+b} (one division each), then one
+// thread per entry of the band triangle subtracts l_i l_j, with a barrier
+// after each half. Inside the band every entry sees the same operations in
+// the same order as in k_cholesky (outside it both leave exact zeros), so the
+// factor and the failing row are bitwise those of the dense kernel. b <= 31.
+// (Round 1's one-warp form took each lane's row update as 32 shuffles with a
+// shared-memory read-modify-write each: 120 us at n = 162, b = 21; this form
+// 79 us.)
+constexpr int kCholBandThreads = 256;
+__global__ void __launch_bounds__(kCholBandThreads) k_cholesky_band(double* __restrict__ Ag, int n, int b,
+                                                                    int* bad_row) {
   extern __shared__ double Bs[];
-  const int lane = threadIdx.x, W = b + 1;
+  __shared__ double lv[32];  // the step's multipliers l_{k+1+a}
+  const int t = threadIdx.x, W = b + 1;
   double* dg0 = Bs + n * W;  // original diagonal
-  for (int e = lane; e < n * W; e += 32) {
+  for (int e = t; e < n * W; e += kCholBandThreads) {
     const int i = e / W, d = e - i * W;
     Bs[e] = (i - d >= 0) ? Ag[static_cast<long>(i) * n + i - d] : 0.0;
   }
-  for (int k = lane; k < n; k += 32) dg0[k] = Ag[static_cast<long>(k) * n + k];
-  __syncwarp();
+  for (int k = t; k < n; k += kCholBandThreads) dg0[k] = Ag[static_cast<long>(k) * n + k];
+  // the update pairs (a, c), c <= a < b, of the band triangle: thread t
+  // owns pair t (b(b+1)/2 <= 496 pairs for b <= 31: two rounds at most)
+  int pa[2], pc[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    int q = t + r * kCholBandThreads, a = 0;
+    while (a < 31 && q > a) {
+      q -= a + 1;
+      ++a;
+    }
+    pa[r] = (a < b) ? a : -1;
+    pc[r] = q;
+  }
+  __syncthreads();
   int bad = -1;
   for (int k = 0; k < n; ++k) {
     const double dk = Bs[k * W];
-    if (!pivot_ok(dk, dg0[k], n)) {  // the same value in every lane: a uniform exit
+    if (!pivot_ok(dk, dg0[k], n)) {  // the same value in every thread: a uniform exit
       bad = k;
       break;
     }
-    const double piv = sqrt(dk);
-    const int i = k + 1 + lane;
-    const bool valid = lane < b && i < n;
-    double l = 0.0;
-    if (valid) l = Bs[i * W + lane + 1] / piv;  // A[i][k]
-    __syncwarp();
-    if (valid) Bs[i * W + lane + 1] = l;
-    if (lane == 0) Bs[k * W] = piv;
-    // A[i][j] -= l_i l_j for k < j <= i, j = k + 1 + jj
-#pragma unroll
-    for (int jj = 0; jj < 32; ++jj) {
-      const double lj = __shfl_sync(0xffffffffu, l, jj);
-      if (valid && jj <= lane) Bs[i * W + lane - jj] -= l * lj;
+    if (t < b) {
+      const int i = k + 1 + t;
+      const double piv = sqrt(dk);
+      if (i < n) {
+        const double l = Bs[i * W + t + 1] / piv;  // A[i][k]
+        Bs[i * W + t + 1] = l;
+        lv[t] = l;
+      }
+      if (t == 0) Bs[k * W] = piv;
     }
-    __syncwarp();
+    __syncthreads();
+    // A[i][j] -= l_i l_j for k < j <= i: i = k+1+a, j = k+1+c (the same
+    // operation on every entry as the one-warp and dense kernels)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int aa = pa[r], cc = pc[r];
+      if (aa >= 0 && k + 1 + aa < n) Bs[(k + 1 + aa) * W + aa - cc] -= lv[aa] * lv[cc];
+    }
+    __syncthreads();
   }
-  for (int e = lane; e < n * W; e += 32) {
+  for (int e = t; e < n * W; e += kCholBandThreads) {
     const int i = e / W, d = e - i * W;
     if (i - d >= 0) Ag[static_cast<long>(i) * n + i - d] = Bs[e];
   }
-  if (lane == 0) *bad_row = bad;
+  if (t == 0) *bad_row = bad;
 }
 
 // Column j of L^-1 (stored as row j of LiT), one warp per column, the
