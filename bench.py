@@ -512,6 +512,24 @@ def launch_ranks(n):
     return subprocess.call(cmd)
 
 
+def arm_watchdog():
+    """A rank that has not finished after TMG_BENCH_WATCHDOG_S seconds (default
+    1800) exits with code 124 and a message instead of waiting forever on a
+    peer: multi-rank NCCL runs of the solver have not been exercised on a
+    multi-GPU box yet (every gpurun box has one GPU), so a hang there ends the
+    rank rather than the driver's whole time slot."""
+    limit = float(os.environ.get("TMG_BENCH_WATCHDOG_S", "1800"))
+
+    def fire():
+        print(f"[bench] rank {dist_env()[1]}: no result after {limit:.0f} s, exiting (watchdog)", file=sys.stderr,
+              flush=True)
+        os._exit(124)
+
+    t = threading.Timer(limit, fire)
+    t.daemon = True
+    t.start()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -524,6 +542,8 @@ def main():
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return launch_ranks(args.gpus)
     ws = dist_env()[0]
+    if ws > 1:
+        arm_watchdog()
     if ws != args.gpus:
         print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={ws}: running {ws} ranks", file=sys.stderr, flush=True)
     if args.impl == "reference":

@@ -50,3 +50,18 @@ def test_gpus_flag_launches_one_rank_per_gpu():
     err = p.stderr
     assert "launching 2 ranks" in err
     assert "rank 0/2" in err and "rank 1/2" in err
+
+
+def test_multi_rank_watchdog_ends_a_stuck_rank():
+    """A rank with no result after TMG_BENCH_WATCHDOG_S exits 124 with a message
+    (bench.arm_watchdog, armed for every rank of an N > 1 run)."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import sys, time; sys.path.insert(0, %r); import bench; bench.arm_watchdog(); time.sleep(30)"
+            % str(ROOT))
+    env = dict(os.environ, TMG_BENCH_WATCHDOG_S="0.5", RANK="1")
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=60, env=env)
+    assert p.returncode == 124
+    assert "rank 1: no result after" in p.stderr
