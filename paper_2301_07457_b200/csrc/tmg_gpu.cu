@@ -1658,6 +1658,20 @@ void setup(H* h, double omega) {
     CKL();
     h->count(2);
   }
+  // the explicit inverse is queued behind the factor before the host reads
+  // the pivot check (a failed factor's inverse is never used: setup throws)
+  for (Rank* R : h->ranks) {
+    const int n = R->n0;
+    const int wpb = 4;
+    const size_t sm = sizeof(double) * n * wpb;
+    CK(cudaFuncSetAttribute(k_lower_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    k_lower_inverse<<<(n + wpb - 1) / wpb, 32 * wpb, sm, h->stream>>>(R->A0, R->LiT, n,
+                                                                       coarsest_band(R->lev[0].g, n));
+    CKL();
+    k_gram<<<dim3((n + 127) / 128, n), 128, 0, h->stream>>>(R->LiT, R->Ainv, n);
+    CKL();
+    h->count(2);
+  }
   for (Rank* R : h->ranks) {
     k_readback<<<1, 1, 0, h->stream>>>(R->bad_row, nullptr, nullptr, R->rbk_dev);
     CKL();
@@ -1670,18 +1684,6 @@ void setup(H* h, double omega) {
       fail(TMG_ERR_DEFINITENESS,
            "matrix is not positive definite: non-positive pivot at row " + std::to_string(bad), bad);
     }
-  }
-  for (Rank* R : h->ranks) {
-    const int n = R->n0;
-    const int wpb = 4;
-    const size_t sm = sizeof(double) * n * wpb;
-    CK(cudaFuncSetAttribute(k_lower_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-    k_lower_inverse<<<(n + wpb - 1) / wpb, 32 * wpb, sm, h->stream>>>(R->A0, R->LiT, n,
-                                                                       coarsest_band(R->lev[0].g, n));
-    CKL();
-    k_gram<<<dim3((n + 127) / 128, n), 128, 0, h->stream>>>(R->LiT, R->Ainv, n);
-    CKL();
-    h->count(2);
   }
   h->have_setup = true;
 }
