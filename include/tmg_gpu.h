@@ -61,8 +61,11 @@ typedef struct tmg_gpu_handle tmg_gpu_handle;
  * num_coarsenings >= 0, divisibility by 2^num_coarsenings. dofs_per_node must
  * be 2 (plane elasticity). device = CUDA ordinal. Limit (no reference twin):
  * the coarsest level, solved through a dense explicit inverse, may have at
- * most 2048 dofs, i.e. 2 (nx/2^nc + 1)(ny/2^nc + 1) <= 2048 (ConfigError
- * otherwise; every BASELINE configuration coarsens to 8x8 = 162 dofs). */
+ * most 16900 dofs, i.e. 2 (nx/2^nc + 1)(ny/2^nc + 1) <= 16900 (ConfigError
+ * otherwise). Every BASELINE configuration coarsens to 8x8 = 162 dofs; the
+ * reference default num_coarsenings = 2 (solvers.hpp:25) stays inside the
+ * limit up to 256x256 or 512x256 elements. Above 2048 dofs the band is
+ * factored in L2 and the handle holds three dense n x n arrays. */
 int tmg_gpu_create(int nx, int ny, int num_coarsenings, int dofs_per_node,
                    int device, tmg_gpu_handle** out);
 void tmg_gpu_destroy(tmg_gpu_handle* h);

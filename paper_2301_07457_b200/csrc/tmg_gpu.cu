@@ -735,6 +735,9 @@ void alloc_rank(H* h, Rank& R) {
   const Grid& g0 = R.lev[0].g;
   R.n0 = 2 * (g0.nx + 1) * (g0.ny + 1);
   const size_t n0sq = sizeof(double) * R.n0 * R.n0;
+  // k_coarse_solve stages the right-hand side in shared memory (one limit for every handle)
+  CK(cudaFuncSetAttribute(k_coarse_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(sizeof(double) * kCoarsestMaxDofs)));
   CK(cudaMalloc(&R.A0, n0sq));
   CK(cudaMalloc(&R.LiT, n0sq));
   CK(cudaMalloc(&R.Ainv, n0sq));
@@ -1585,6 +1588,7 @@ void finish_update(H* h, int it) {
 // away is (x-1, y-1), ny + 2 nodes back).
 int coarsest_band(const Grid& g0, int n) { return std::min(n - 1, 2 * (g0.ny + 2) + 1); }
 
+
 // dense Cholesky of the coarsest matrix, in shared memory when it fits
 void launch_cholesky(cudaStream_t s, double* A, int n, int* bad_row) {
   if (n <= kCholSmemMax) {
@@ -1649,7 +1653,11 @@ void setup(H* h, double omega) {
     CKL();
     const int b = coarsest_band(g0, n);
     const size_t bsm = static_cast<size_t>(n) * (b + 2) * sizeof(double);
-    if (h->band_factor && b <= 31 && bsm <= 200 * 1024) {
+    if (n > kDenseFactorMaxDofs) {
+      // large coarsest level: the band is factored in place in L2 (LiT's
+      // first row is the scratch for the original diagonal)
+      k_cholesky_band_g<<<1, kCholBandGThreads, sizeof(double) * b, h->stream>>>(R->A0, n, b, R->LiT, R->bad_row);
+    } else if (h->band_factor && b <= 31 && bsm <= 200 * 1024) {
       CK(cudaFuncSetAttribute(k_cholesky_band, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bsm)));
       k_cholesky_band<<<1, kCholBandThreads, bsm, h->stream>>>(R->A0, n, b, R->bad_row);
     } else {
@@ -1662,6 +1670,20 @@ void setup(H* h, double omega) {
   // the pivot check (a failed factor's inverse is never used: setup throws)
   for (Rank* R : h->ranks) {
     const int n = R->n0;
+    if (n > kDenseFactorMaxDofs) {
+      const int b = coarsest_band(R->lev[0].g, n);
+      int RW = 32;
+      while (RW < b + 1) RW *= 2;
+      const int wpb = 8;
+      k_lower_inverse_band<<<(n + wpb - 1) / wpb, 32 * wpb, sizeof(double) * RW * wpb, h->stream>>>(R->A0, R->LiT, n,
+                                                                                                     b, RW);
+      CKL();
+      const int nt = (n + kGramTile - 1) / kGramTile;
+      k_gram_tiled<<<dim3(nt, nt), 256, 0, h->stream>>>(R->LiT, R->Ainv, n);
+      CKL();
+      h->count(2);
+      continue;
+    }
     const int wpb = 4;
     const size_t sm = sizeof(double) * n * wpb;
     CK(cudaFuncSetAttribute(k_lower_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
@@ -1918,9 +1940,9 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
     return cfg("ny = " + std::to_string(ny) + " is not divisible by 2^" + std::to_string(nc) + " = " +
                std::to_string(factor));
   const int n0 = 2 * (nx / factor + 1) * (ny / factor + 1);
-  if (n0 > 2048) {
-    return cfg("coarsest level has " + std::to_string(n0) +
-               " dofs; the device coarse solve supports <= 2048 (add coarsenings)");
+  if (n0 > kCoarsestMaxDofs) {
+    return cfg("coarsest level has " + std::to_string(n0) + " dofs; the device coarse solve supports <= " +
+               std::to_string(kCoarsestMaxDofs) + " (add coarsenings)");
   }
   if (nranks < 1 || rank < 0 || rank >= nranks) return cfg("invalid rank / nranks");
   hp->device = device;

@@ -686,6 +686,153 @@ __global__ void __launch_bounds__(kCholBandThreads) k_cholesky_band(double* __re
   if (t == 0) *bad_row = bad;
 }
 
+// Coarsest levels up to kDenseFactorMaxDofs dofs take the one-CTA factor
+// kernels (dense, or the band in shared memory); larger ones, up to
+// kCoarsestMaxDofs (three dense n x n arrays: 2.3 GB each at the limit),
+// factor the band in L2 and form the explicit inverse with the banded /
+// tiled kernels (k_cholesky_band_g, k_lower_inverse_band, k_gram_tiled).
+constexpr int kDenseFactorMaxDofs = 2048;
+constexpr int kCoarsestMaxDofs = 16900;
+
+// Banded Cholesky of a large coarsest matrix (n > 2048: reference configs
+// with few coarsenings, e.g. 256^2 with the default num_coarsenings = 2,
+// solvers.hpp:25), in place on the band of the dense row-major matrix, one
+// CTA. The band (n (b + 1) doubles, a few MB) lives in L2; step k forms the
+// b multipliers (one thread each, kept in shared memory) and then one warp
+// per row of the band triangle subtracts l_i l_j along the row. The same
+// operation on every entry in the same order as k_cholesky / k_cholesky_band.
+// dg0: n doubles of scratch for the original diagonal (pivot_ok).
+constexpr int kCholBandGThreads = 1024;
+__global__ void __launch_bounds__(kCholBandGThreads) k_cholesky_band_g(double* A, int n, int b, double* dg0,
+                                                                       int* bad_row) {
+  extern __shared__ double lvg[];  // b multipliers
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  constexpr int nw = kCholBandGThreads / 32;
+  for (int k = t; k < n; k += kCholBandGThreads) dg0[k] = A[static_cast<long>(k) * n + k];
+  __syncthreads();
+  int bad = -1;
+  for (int k = 0; k < n; ++k) {
+    const double dk = A[static_cast<long>(k) * n + k];
+    if (!pivot_ok(dk, dg0[k], n)) {  // the same value in every thread: a uniform exit
+      bad = k;
+      break;
+    }
+    const double piv = sqrt(dk);
+    const int m = min(b, n - 1 - k);  // rows below the pivot inside the band
+    for (int a = t; a < m; a += kCholBandGThreads) {
+      double* p = A + static_cast<long>(k + 1 + a) * n + k;
+      const double l = *p / piv;
+      *p = l;
+      lvg[a] = l;
+    }
+    __syncthreads();  // also orders the read of A[k][k] above before its overwrite below
+    if (t == 0) A[static_cast<long>(k) * n + k] = piv;
+    for (int a = w; a < m; a += nw) {
+      const double la = lvg[a];
+      double* Ai = A + static_cast<long>(k + 1 + a) * n + k + 1;
+      for (int c = lane; c <= a; c += 32) Ai[c] -= la * lvg[c];
+    }
+    __syncthreads();
+  }
+  if (t == 0) *bad_row = bad;
+}
+
+// Column j of L^-1 for a banded L of any half-bandwidth b (large coarsest
+// levels), one warp per column. y_i = -(sum_{k in [max(j, i-b), i)} L_ik y_k)
+// / L_ii only reads the last b entries of the column, which are kept in a
+// shared-memory ring of RW >= b + 1 doubles per warp (RW a power of two), so
+// every column of the matrix has a resident warp at once and the L2 latency
+// of a row is hidden by the other columns. Entries above the diagonal are
+// written as zeros (k_gram and k_coarse_solve read full rows).
+__global__ void k_lower_inverse_band(const double* __restrict__ L, double* __restrict__ LiT, int n, int b,
+                                     int RW) {
+  extern __shared__ double yring[];
+  const int wpb = blockDim.x >> 5;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x * wpb + w;
+  if (j >= n) return;
+  double* yr = yring + static_cast<long>(w) * RW;
+  double* out = LiT + static_cast<long>(j) * n;
+  for (int i = lane; i < j; i += 32) out[i] = 0.0;
+  const double yj = 1.0 / L[static_cast<long>(j) * n + j];
+  if (lane == 0) {
+    yr[j & (RW - 1)] = yj;
+    out[j] = yj;
+  }
+  __syncwarp();
+  for (int i = j + 1; i < n; ++i) {
+    const double* Li = L + static_cast<long>(i) * n;
+    const double dg = Li[i];
+    double s = 0.0;
+    for (int k = max(j, i - b) + lane; k < i; k += 32) s = fma(Li[k], yr[k & (RW - 1)], s);
+    s = warp_sum(s);
+    __syncwarp();  // every lane has read the ring before slot i (= slot i - RW) is rewritten
+    if (lane == 0) {
+      const double yi = -s / dg;
+      yr[i & (RW - 1)] = yi;
+      out[i] = yi;
+    }
+    __syncwarp();
+  }
+}
+
+// Ainv = L^-T L^-1 for large n: 64x64 tiles of the lower triangle (mirrored
+// into the upper one), 4x4 entries per thread, 16 columns of LiT per step
+// staged in shared memory. Every entry sums its products in increasing k by
+// fma like k_gram; the steps before max(i, j) add exact zeros (LiT is upper
+// triangular), so the result is bitwise k_gram's.
+constexpr int kGramTile = 64, kGramK = 16;
+__global__ void __launch_bounds__(256) k_gram_tiled(const double* __restrict__ LiT, double* __restrict__ Ainv,
+                                                    int n) {
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  if (bj > bi) return;
+  __shared__ double As[kGramK][kGramTile + 1];
+  __shared__ double Bs[kGramK][kGramTile + 1];
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int i0 = bi * kGramTile, j0 = bj * kGramTile;
+  double acc[4][4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
+  // rows i >= i0 of LiT are zero left of column i0 (i0 >= j0)
+  for (int k0 = i0 / kGramK * kGramK; k0 < n; k0 += kGramK) {
+    // 64 rows x 16 columns per operand: thread t loads 4 entries of each
+    for (int e = t; e < kGramTile * kGramK; e += 256) {
+      const int r = e / kGramK, kk = e % kGramK;
+      const int k = k0 + kk;
+      const int ia = i0 + r, jb = j0 + r;
+      As[kk][r] = (ia < n && k < n) ? LiT[static_cast<long>(ia) * n + k] : 0.0;
+      Bs[kk][r] = (jb < n && k < n) ? LiT[static_cast<long>(jb) * n + k] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kGramK; ++kk) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        av[p] = As[kk][ty * 4 + p];
+        bv[p] = Bs[kk][tx * 4 + p];
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = fma(av[p], bv[q], acc[p][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + ty * 4 + p, j = j0 + tx * 4 + q;
+      if (i < n && j < n) {
+        Ainv[static_cast<long>(i) * n + j] = acc[p][q];
+        if (bi != bj) Ainv[static_cast<long>(j) * n + i] = acc[p][q];
+      }
+    }
+}
+
 // Column j of L^-1 (stored as row j of LiT), one warp per column, the
 // running column kept in shared memory.
 // b: lower half-bandwidth of L (>= n - 1 when dense); with b <= 31 a row's

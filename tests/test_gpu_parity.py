@@ -506,6 +506,42 @@ def test_specialised_coarse_kernels_are_bitwise(monkeypatch, nx, ny, nc, recipe,
     assert np.array_equal(va, vc)
 
 
+@pytest.mark.parametrize("nx,ny,nc,recipe", [(128, 128, 2, "iid"), (256, 128, 2, "checker"), (256, 256, 2, "iid"),
+                                              (128, 256, 1, "iid")])
+def test_large_coarsest_level_matches_reference(nx, ny, nc, recipe):
+    """Reference configs with few coarsenings (the default num_coarsenings = 2,
+    solvers.hpp:25) leave a coarsest level of thousands of dofs, which
+    CholeskyFactor (solvers.cpp:89-152) accepts at any size. Above 2048 dofs
+    the device factors the band in L2 and forms the explicit inverse with the
+    banded / tiled kernels: same cycle, same solve, same iteration count."""
+    ops, sysc, b, _, _ = pair(nx, ny, nc, recipe, 5)
+    assert 2 * (nx // 2**nc + 1) * (ny // 2**nc + 1) > 2048
+    rng = np.random.default_rng(3)
+    f = rng.standard_normal(sysc.n)
+    got = P.mg_cycle(ops, np.zeros(sysc.n), f, 1, 2, 2)
+    want = sysc.vcycle(f, np.zeros(sysc.n), 1, 2, 2)
+    assert rel(got, want) <= 1e-10
+    cfg = P.SolverConfig(tol=1e-8, max_iter=2000, num_coarsenings=nc)
+    rep = P.pcgmg_solve(ops, b, cfg)
+    ref = sysc.solve(b, tol=1e-8, max_iter=2000)
+    assert rep.converged and ref["converged"]
+    assert abs(rep.iterations - ref["iterations"]) <= 2
+    assert rel(rep.solution, ref["solution"]) <= 1e-8
+    c_ref = sysc.compliance(ref["solution"])
+    assert abs(P.compliance(ops) - c_ref) <= 1e-9 * abs(c_ref)
+
+
+def test_large_coarsest_level_singular_and_limit():
+    """An unconstrained structure fails at the first dependent pivot of the
+    large banded factor too (solvers.cpp:144-148); beyond the documented limit
+    the handle is refused with ConfigError."""
+    free = P.MultigridOperators(P.GridLevel(128, 128), 2, 0.3, P.BoundaryConditions([], []))
+    with pytest.raises(P.DefinitenessError):
+        free.set_moduli(np.ones(128 * 128))
+    with pytest.raises(P.ConfigError):
+        P.MultigridOperators(P.GridLevel(512, 512), 2, 0.3, P.BoundaryConditions([], []))
+
+
 @pytest.mark.parametrize("nx,ny,nc", [(64, 64, 3), (128, 96, 3), (160, 96, 4)])
 def test_banded_coarsest_factor_is_the_dense_one(monkeypatch, nx, ny, nc):
     """The banded one-warp Cholesky of the coarsest matrix performs, inside
