@@ -2481,8 +2481,10 @@ namespace {
 // Scratch of one OC exchange on rank 0: the per-element 32-byte records
 // first (aligned at the allocation base), then maxima, partials, barrier and
 // flags. Grown on demand; `extra` doubles after it are the caller's.
+long oc_records(long ne) { return 4 * ne; }  // doubles: two 16-byte record streams
+
 double* oc_scratch(Rank& R, long ne, long extra, int blocks) {
-  return grow(R.ocbuf, R.ocbuf_cap, 4 * ne + 4L * blocks + 4 + extra);
+  return grow(R.ocbuf, R.ocbuf_cap, oc_records(ne) + 4L * blocks + 4 + extra);
 }
 
 int oc_blocks() {
@@ -2493,6 +2495,8 @@ int oc_blocks() {
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_oc_bisect, kOcThreads, 0));
     if (per_sm < 1) fail(TMG_ERR_CUDA, "k_oc_bisect cannot be resident");
+    // TMG_OC_CTAS: fewer CTAs per SM than the residency limit (for A/B timing)
+    if (const char* e = std::getenv("TMG_OC_CTAS")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
     blocks = sms * per_sm;
   }
   return blocks;
@@ -2510,8 +2514,9 @@ void oc_pair_device(H* h, Rank& R, double* scratch, double* alpha, long ne, int 
   a.np = np;
   a.pa = pa;
   a.pb = pb;
-  a.el = reinterpret_cast<double4*>(scratch);
-  a.pmax = scratch + 4 * ne;
+  a.el0 = reinterpret_cast<double2*>(scratch);
+  a.el1 = a.el0 + ne;
+  a.pmax = scratch + oc_records(ne);
   a.part = a.pmax + 2L * blocks;
   a.bar = reinterpret_cast<unsigned*>(a.part + 2L * blocks);
   a.met = reinterpret_cast<int*>(a.bar + 2);
@@ -2526,6 +2531,8 @@ void oc_pair_device(H* h, Rank& R, double* scratch, double* alpha, long ne, int 
   CK(cudaEventRecord(h->ev[2], h->stream));
   k_oc_prep<<<blocks, kOcThreads, 0, h->stream>>>(a);
   CKL();
+  k_oc_gain<<<blocks, kOcThreads, 0, h->stream>>>(a, blocks);
+  CKL();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(blocks);
   cfg.blockDim = dim3(kOcThreads);
@@ -2537,7 +2544,7 @@ void oc_pair_device(H* h, Rank& R, double* scratch, double* alpha, long ne, int 
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, k_oc_bisect, a, blocks));
   CK(cudaEventRecord(h->ev[3], h->stream));
-  h->count(2);
+  h->count(3);
   int* flags = reinterpret_cast<int*>(R.scal_host);
   CK(cudaMemcpyAsync(flags, a.met, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
@@ -2570,7 +2577,7 @@ int tmg_gpu_oc_update_pair(tmg_gpu_handle* h, double* alpha, int nphases, double
     // scratch, then the uploaded density, sens a/b and move
     const int blocks = oc_blocks();
     double* scratch = oc_scratch(R, ne, ne * nphases + 3 * ne, blocks);
-    double* d_alpha = scratch + 4 * ne + 4L * blocks + 4;
+    double* d_alpha = scratch + oc_records(ne) + 4L * blocks + 4;
     double* sa = d_alpha + ne * nphases;
     double* sb = sa + ne;
     double* mv = sb + ne;

@@ -5,16 +5,18 @@
 // passes, each a clamp(a * (max(floor, gain) / lambda)^damping) (or a clamp of
 // a uniform shift when no element prefers phase a) followed by the mean. Here
 //   k_oc_prep   reads the element-major density once (phases a, b), forms
-//               {a, lo, hi, gain} per element in scratch and the per-CTA
-//               maxima of gain and of the move limit;
+//               {a, gain} and {lo, hi} per element in scratch (two 16-byte
+//               streams) and the per-CTA maxima of gain and of the move limit;
+//   k_oc_gain   turns gain into the lambda-independent factor once the
+//               global maximum is known (multiplicative branch);
 //   k_oc_bisect runs the whole bisection in one cooperatively launched
 //               persistent grid: per step every CTA reduces its elements,
 //               publishes one partial, crosses a grid barrier and sums the
 //               partials in index order itself, so every CTA takes the same
 //               (deterministic) branch; at the end it writes phases a and b
 //               back into the element-major density.
-// Bytes per element and step: {a, lo, hi, gain} = 32 in one interleaved
-// stream (the reference streams the same plus its cand write).
+// Bytes per element and step: {a, gain, lo, hi} = 32 (the reference streams
+// the same plus its cand write).
 #pragma once
 
 #include <cstdint>
@@ -25,6 +27,7 @@
 namespace tmg {
 
 constexpr int kOcThreads = 256;
+constexpr unsigned kOcMaxStaged = 1536;  // step partials staged in shared memory (148 SMs x 8 CTAs = 1184)
 
 struct OcArgs {
   long ne;
@@ -37,7 +40,11 @@ struct OcArgs {
   double eps;        // density floor
   double target;
   double damping;
-  double4* el;       // scratch per element: {alpha_a, lo, hi, gain} (one 32-byte stream)
+  // scratch per element as two 16-byte streams, {alpha_a, gain} and {lo, hi}:
+  // a warp's load of either is 512 contiguous bytes (one 32-byte record per
+  // element read as two 16-byte halves used half of every sector per request)
+  double2* el0;
+  double2* el1;
   double* pmax;      // per-CTA [max gain, max move] (prep) -> 2 * gridDim
   double* part;      // per-CTA step partials, 2 * gridDim (double-buffered)
   unsigned* bar;     // grid barrier [arrivals, generation]
@@ -58,7 +65,8 @@ __global__ void __launch_bounds__(kOcThreads) k_oc_prep(OcArgs a) {
     const double pair = x + a.alpha[e * a.np + a.pb];
     mg = s_max(mg, g);
     mm = s_max(mm, m);
-    a.el[e] = make_double4(x, s_max(a.eps, x - m), s_min(pair - a.eps, x + m), g);
+    a.el0[e] = make_double2(x, g);
+    a.el1[e] = make_double2(s_max(a.eps, x - m), s_min(pair - a.eps, x + m));
   }
   // block maxima (max is exact in any order)
   __shared__ double smg[kOcThreads], smm[kOcThreads];
@@ -108,50 +116,114 @@ struct OcStep {
   double scale;   // 1/sqrt(lambda) (half) or log(lambda)
   double damping;
 };
+template <int MODE>  // 0: uniform shift, 1: damping 0.5, 2: any damping
 __device__ __forceinline__ double oc_cand(const double4 v, const OcStep& s) {
   // v = {alpha_a, lo, hi, q}
-  if (s.shift) return s_clamp(v.x + s.t, v.y, v.z);
-  const double p = s.half ? v.w * s.scale : exp(s.damping * (v.w - s.scale));
+  if (MODE == 0) return s_clamp(v.x + s.t, v.y, v.z);
+  const double p = (MODE == 1) ? v.w * s.scale : exp(s.damping * (v.w - s.scale));
   return s_clamp(v.x * p, v.y, v.z);
 }
-// plain L2-coherent loads (ld.global.cg), not the read-only path: the kernel
-// itself rewrites the gain word of every record before the bisection steps
-__device__ __forceinline__ double4 ld_el(const double4* p) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-  const double2 u = __ldcg(q), w = __ldcg(q + 1);
-  return make_double4(u.x, u.y, w.x, w.y);
+// The records are read-only inside k_oc_bisect (k_oc_gain, a launch of its
+// own, finishes them), so they go through the non-coherent path and the
+// compiler is free to issue a whole batch of loads before the first use
+// (__ldcg is an asm volatile: the loads kept their program order between the
+// candidates and only three or four were in flight per thread).
+__device__ __forceinline__ double4 ld_el(const double2* __restrict__ el0, const double2* __restrict__ el1, long e) {
+  const double2 u = __ldg(el0 + e), w = __ldg(el1 + e);
+  return make_double4(u.x, w.x, w.y, u.y);
 }
 
-__global__ void __launch_bounds__(kOcThreads) k_oc_bisect(OcArgs a, int prep_blocks) {
-  __shared__ double red[kOcThreads / 32];
-  __shared__ double s_mean;
-  __shared__ unsigned s_gen;
-  if (threadIdx.x == 0) s_gen = *reinterpret_cast<volatile unsigned*>(a.bar + 1);
-  // global maxima from the prep partials (identical in every CTA)
-  double max_gain = -1e300, max_move = 0.0;
+// global maxima of gain and move limit from the prep partials
+__device__ __forceinline__ void oc_maxima(const OcArgs& a, int prep_blocks, double& max_gain, double& max_move) {
+  max_gain = -1e300;
+  max_move = 0.0;
   for (int k = 0; k < prep_blocks; ++k) {
     max_gain = s_max(max_gain, __ldcg(a.pmax + 2 * k));
     max_move = s_max(max_move, __ldcg(a.pmax + 2 * k + 1));
   }
+}
+
+// The lambda-independent part of every element's factor (multiplicative
+// branch): gain -> sqrt(max(floor, gain)) for damping 0.5, else its log.
+__global__ void __launch_bounds__(kOcThreads) k_oc_gain(OcArgs a, int prep_blocks) {
+  double max_gain, max_move;
+  oc_maxima(a, prep_blocks, max_gain, max_move);
+  if (!(max_gain > 0.0)) return;  // shift branch: the gain is not used
+  const double floor_gain = 1e-4 * max_gain;
+  const bool half = a.damping == 0.5;
+  for (long e = blockIdx.x * static_cast<long>(kOcThreads) + threadIdx.x; e < a.ne;
+       e += static_cast<long>(gridDim.x) * kOcThreads) {
+    const double g = s_max(floor_gain, a.el0[e].y);
+    a.el0[e].y = half ? sqrt(g) : log(g);
+  }
+}
+
+// One bisection step's sum over the elements a thread owns: kOcU records
+// (2 kOcU 16-byte loads) issued as one batch per round, one partial sum per
+// slot, a fixed pairwise tree at the end (deterministic). The mode is a
+// template argument so the common damping-0.5 loop carries no exp()
+// registers. The kernel is bound by loads in flight (ncu: > 90 % of cycles
+// without an eligible warp), and its speed follows the compiler's schedule
+// of that batch: at 80 registers and three CTAs per SM the eight loads go
+// out back to back and the kernel streams at 0.83 of the DRAM peak (ncu);
+// tighter register caps (48, 40) serialise part of the batch behind the
+// first candidates (0.54-0.63 of HBM end to end), and eight records per
+// round or a CTA-contiguous element order were slower as well (same-box A/B,
+// tools/ab_oc.sh). A shared-memory ring filled by bulk copies (one producer
+// warp, 512-element entries) was correct but slower still (10.5-12.7 ms
+// against 7.5 ms at 8192^2): with two elements per thread and ring entry the
+// mbarrier hand-off dominates.
+#ifndef TMG_OC_U
+#define TMG_OC_U 4
+#endif
+#ifndef TMG_OC_MINB
+#define TMG_OC_MINB 3
+#endif
+constexpr int kOcU = TMG_OC_U;
+template <int MODE>
+__device__ __forceinline__ double oc_step_sum(const double2* __restrict__ el0, const double2* __restrict__ el1,
+                                              long ne, const OcStep& st, long e, long stride) {
+  double s[kOcU];
+#pragma unroll
+  for (int k = 0; k < kOcU; ++k) s[k] = 0.0;
+#pragma unroll 1
+  for (; e + (kOcU - 1) * stride < ne; e += kOcU * stride) {
+    double4 v[kOcU];
+#pragma unroll
+    for (int k = 0; k < kOcU; ++k) v[k] = ld_el(el0, el1, e + k * stride);
+#pragma unroll
+    for (int k = 0; k < kOcU; ++k) s[k] += oc_cand<MODE>(v[k], st);
+  }
+#pragma unroll 1
+  for (; e < ne; e += stride) s[0] += oc_cand<MODE>(ld_el(el0, el1, e), st);
+#pragma unroll
+  for (int w = 1; w < kOcU; w *= 2)
+#pragma unroll
+    for (int k = 0; k + w < kOcU; k += 2 * w) s[k] += s[k + w];
+  return s[0];
+}
+
+__global__ void __launch_bounds__(kOcThreads, TMG_OC_MINB) k_oc_bisect(OcArgs a, int prep_blocks) {
+  __shared__ double red[kOcThreads / 32];
+  __shared__ double sparts[kOcMaxStaged];
+  __shared__ double s_mean;
+  __shared__ unsigned s_gen;
+  if (threadIdx.x == 0) s_gen = *reinterpret_cast<volatile unsigned*>(a.bar + 1);
+  // global maxima from the prep partials (identical in every CTA)
+  double max_gain, max_move;
+  oc_maxima(a, prep_blocks, max_gain, max_move);
+  const double2* __restrict__ el0 = a.el0;
+  const double2* __restrict__ el1 = a.el1;
   __syncthreads();
   unsigned gen = s_gen;
   OcStep st{};
   st.shift = !(max_gain > 0.0);  // mto.cpp:170: max_gain <= 0
   st.half = a.damping == 0.5;
   st.damping = a.damping;
-  const double floor_gain = 1e-4 * max_gain;
   const double vol_tol = 1e-6;
   double t_lo = -max_move, t_hi = max_move, l_lo = 1e-10, l_hi = 1e10;
   bool met = false;
   const long stride = static_cast<long>(gridDim.x) * kOcThreads;
-  if (!st.shift) {
-    // the lambda-independent part of every element's factor, on the elements
-    // this thread owns in every step
-    for (long e = blockIdx.x * static_cast<long>(kOcThreads) + threadIdx.x; e < a.ne; e += stride) {
-      const double g = s_max(floor_gain, a.el[e].w);
-      a.el[e].w = st.half ? sqrt(g) : log(g);
-    }
-  }
   for (int it = 0; it <= 100; ++it) {
     if (st.shift) {
       st.t = 0.5 * (t_lo + t_hi);
@@ -160,19 +232,10 @@ __global__ void __launch_bounds__(kOcThreads) k_oc_bisect(OcArgs a, int prep_blo
       st.scale = st.half ? 1.0 / sqrt(lambda) : log(lambda);
       st.t = lambda;  // kept for the bound update below
     }
-    // four independent partial sums per thread (fixed order: deterministic)
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    long e = blockIdx.x * static_cast<long>(kOcThreads) + threadIdx.x;
-    for (; e + 3 * stride < a.ne; e += 4 * stride) {
-      const double4 v0 = ld_el(a.el + e), v1 = ld_el(a.el + e + stride), v2 = ld_el(a.el + e + 2 * stride),
-                    v3 = ld_el(a.el + e + 3 * stride);
-      s0 += oc_cand(v0, st);
-      s1 += oc_cand(v1, st);
-      s2 += oc_cand(v2, st);
-      s3 += oc_cand(v3, st);
-    }
-    for (; e < a.ne; e += stride) s0 += oc_cand(ld_el(a.el + e), st);
-    double s = (s0 + s1) + (s2 + s3);
+    const long e0 = blockIdx.x * static_cast<long>(kOcThreads) + threadIdx.x;
+    double s = st.shift ? oc_step_sum<0>(el0, el1, a.ne, st, e0, stride)
+                        : (st.half ? oc_step_sum<1>(el0, el1, a.ne, st, e0, stride)
+                                   : oc_step_sum<2>(el0, el1, a.ne, st, e0, stride));
     // fixed-shape block tree
     for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
@@ -183,9 +246,22 @@ __global__ void __launch_bounds__(kOcThreads) k_oc_bisect(OcArgs a, int prep_blo
       a.part[(it & 1) * gridDim.x + blockIdx.x] = b;
     }
     oc_grid_sync(a.bar, gen);
+    // every CTA sums all partials in index order. The block first stages them
+    // in shared memory with one coalesced load: thread 0 reading them from L2
+    // one after another put load latency on every step.
+    const double* parts = a.part + (it & 1) * gridDim.x;
+    const bool staged = gridDim.x <= kOcMaxStaged;
+    if (staged) {
+      for (unsigned k = threadIdx.x; k < gridDim.x; k += kOcThreads) sparts[k] = __ldcg(parts + k);
+      __syncthreads();
+    }
     if (threadIdx.x == 0) {
       double sum = 0.0;
-      for (unsigned k = 0; k < gridDim.x; ++k) sum += __ldcg(a.part + (it & 1) * gridDim.x + k);
+      if (staged) {
+        for (unsigned k = 0; k < gridDim.x; ++k) sum += sparts[k];
+      } else {
+        for (unsigned k = 0; k < gridDim.x; ++k) sum += __ldcg(parts + k);
+      }
       s_mean = sum / static_cast<double>(a.ne);
     }
     __syncthreads();
@@ -201,8 +277,8 @@ __global__ void __launch_bounds__(kOcThreads) k_oc_bisect(OcArgs a, int prep_blo
   if (blockIdx.x == 0 && threadIdx.x == 0) a.met[0] = met ? 1 : 0;
   if (!met) return;
   for (long e = blockIdx.x * static_cast<long>(kOcThreads) + threadIdx.x; e < a.ne; e += stride) {
-    const double4 v = ld_el(a.el + e);
-    const double c = oc_cand(v, st);
+    const double4 v = ld_el(el0, el1, e);
+    const double c = st.shift ? oc_cand<0>(v, st) : (st.half ? oc_cand<1>(v, st) : oc_cand<2>(v, st));
     const double pair = v.x + a.alpha[e * a.np + a.pb];
     a.alpha[e * a.np + a.pa] = c;
     a.alpha[e * a.np + a.pb] = pair - c;

@@ -444,7 +444,13 @@ void p_setup(PH* h, double omega) {
   CK(cudaMemsetAsync(h->A0, 0, sizeof(double) * n * n, h->stream));
   k_p_dense<<<p_grid(C.g), kPT, 0, h->stream>>>(C.S, C.g, h->A0, n);
   CKL();
-  launch_cholesky(h->stream, h->A0, n, h->bad_row);
+  // 1 dof per node: the farthest lower neighbour (x-1, y-1) is ny + 2 back
+  const int band = std::min(n - 1, C.g.ny + 2);
+  const bool large = n > kDenseFactorMaxDofs;  // as on the elasticity handle (tmg_kernels.cuh)
+  if (large)
+    k_cholesky_band_g<<<1, kCholBandGThreads, sizeof(double) * band, h->stream>>>(h->A0, n, band, h->LiT, h->bad_row);
+  else
+    launch_cholesky(h->stream, h->A0, n, h->bad_row);
   CKL();
   int bad = -1;
   CK(cudaMemcpyAsync(&bad, h->bad_row, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
@@ -452,13 +458,25 @@ void p_setup(PH* h, double omega) {
   if (bad >= 0)
     fail(TMG_ERR_DEFINITENESS, "matrix is not positive definite: non-positive pivot at row " + std::to_string(bad),
          bad);
-  const int wpb = 4;
-  const size_t sm = sizeof(double) * n * wpb;
-  CK(cudaFuncSetAttribute(k_lower_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-  k_lower_inverse<<<(n + wpb - 1) / wpb, 32 * wpb, sm, h->stream>>>(h->A0, h->LiT, n, n);
-  CKL();
-  k_gram<<<dim3((n + 127) / 128, n), 128, 0, h->stream>>>(h->LiT, h->Ainv, n);
-  CKL();
+  if (large) {
+    int RW = 32;
+    while (RW < band + 1) RW *= 2;
+    const int wpb = 8;
+    k_lower_inverse_band<<<(n + wpb - 1) / wpb, 32 * wpb, sizeof(double) * RW * wpb, h->stream>>>(h->A0, h->LiT, n,
+                                                                                                   band, RW);
+    CKL();
+    const int nt = (n + kGramTile - 1) / kGramTile;
+    k_gram_tiled<<<dim3(nt, nt), 256, 0, h->stream>>>(h->LiT, h->Ainv, n);
+    CKL();
+  } else {
+    const int wpb = 4;
+    const size_t sm = sizeof(double) * n * wpb;
+    CK(cudaFuncSetAttribute(k_lower_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    k_lower_inverse<<<(n + wpb - 1) / wpb, 32 * wpb, sm, h->stream>>>(h->A0, h->LiT, n, n);
+    CKL();
+    k_gram<<<dim3((n + 127) / 128, n), 128, 0, h->stream>>>(h->LiT, h->Ainv, n);
+    CKL();
+  }
   CK(cudaStreamSynchronize(h->stream));
   h->have_setup = true;
 }
@@ -482,7 +500,9 @@ int tmg_poisson_create(int nx, int ny, int num_coarsenings, int device, tmg_pois
   h->nc = num_coarsenings;
   const int st = p_guarded(h, [&] {
     const int n0 = ((nx >> num_coarsenings) + 1) * ((ny >> num_coarsenings) + 1);
-    if (n0 > 2048) fail(TMG_ERR_CONFIG, "coarsest level has " + std::to_string(n0) + " dofs; at most 2048");
+    if (n0 > kCoarsestMaxDofs)
+      fail(TMG_ERR_CONFIG, "coarsest level has " + std::to_string(n0) + " dofs; at most " +
+                               std::to_string(kCoarsestMaxDofs));
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->lev.resize(num_coarsenings + 1);
     for (int l = 0; l <= num_coarsenings; ++l) {

@@ -117,3 +117,24 @@ def test_random_source_warm_start_and_errors():
         ops.solve(b, P.SolverConfig(pre_sweeps=1, post_sweeps=2))
     with pytest.raises(P.ConfigError):
         P.PoissonMultigrid(P.GridLevel(12, 12), 3)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("g,nc", [(128, 1), (256, 2), (256, 1)])
+def test_large_coarsest_level(g, nc):
+    """Few coarsenings leave a coarsest level above 2048 dofs, which the
+    reference's CholeskyFactor accepts (solvers.cpp:89-152): the large banded
+    factor / tiled inverse path gives the reference's count and solution."""
+    assert ((g >> nc) + 1) ** 2 > 2048
+    grid = P.GridLevel(g, g)
+    ops = P.PoissonMultigrid(grid, nc)
+    b = P.assemble_poisson_rhs(grid, 1.0)
+    rep = ops.solve(b, P.SolverConfig(tol=1e-8, max_iter=500, num_coarsenings=nc))
+    sysc = po.poisson_system("orc", g, g, 1.0).build_mg(nc, 0.6)
+    ref = sysc.solve(b, tol=1e-8, max_iter=500)
+    assert rep.converged and ref["converged"]
+    assert abs(rep.iterations - ref["iterations"]) <= 2
+    assert rel(rep.solution, ref["solution"]) <= 1e-8
+    rng = np.random.default_rng(g)
+    f = rng.standard_normal((g + 1) ** 2)
+    assert rel(ops.vcycle(np.zeros_like(f), f, 1, 2, 2), sysc.vcycle(f, np.zeros_like(f), 1, 2, 2)) <= 1e-11
