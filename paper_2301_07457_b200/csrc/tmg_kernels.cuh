@@ -89,8 +89,19 @@ __device__ __forceinline__ double fixed_sum(const double* p, int n) {
   __shared__ double sh[4];
   const int t = threadIdx.x + threadIdx.y * blockDim.x;
   if (t < 128) {
+    // eight loads in flight per lane (__ldcg is an asm volatile: one add per
+    // load would expose an L2 round trip every few elements); the adds keep
+    // the lane's increasing-k order, so the sum is bitwise unchanged
     double acc = 0.0;
-    for (int k = t; k < n; k += 128) acc += __ldcg(p + k);
+    int k = t;
+    for (; k + 7 * 128 < n; k += 8 * 128) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldcg(p + k + j * 128);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc += v[j];
+    }
+    for (; k < n; k += 128) acc += __ldcg(p + k);
     acc = warp_sum(acc);
     if ((t & 31) == 0) sh[t >> 5] = acc;
   }
