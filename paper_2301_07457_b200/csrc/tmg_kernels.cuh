@@ -957,11 +957,16 @@ __global__ void __launch_bounds__(kCoarseSolveThreads) k_coarse_solve(const doub
   const int lane = threadIdx.x & 31;
   const int node = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (node >= nodes) return;
+  // Ainv is bitwise symmetric (k_gram forms (i, j) and (j, i) with the same
+  // operations), so the node's two columns are read as its two rows: the
+  // same values in the same order, contiguous across the lanes
+  const double* r0 = Ainv + static_cast<long>(2 * node) * n;
+  const double* r1 = r0 + n;
   double s0 = 0.0, s1 = 0.0;
   for (int k = lane; k < n; k += 32) {
     const double fk = fd[k];
-    s0 = fma(Ainv[static_cast<long>(k) * n + 2 * node], fk, s0);
-    s1 = fma(Ainv[static_cast<long>(k) * n + 2 * node + 1], fk, s1);
+    s0 = fma(r0[k], fk, s0);
+    s1 = fma(r1[k], fk, s1);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
