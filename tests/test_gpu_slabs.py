@@ -32,6 +32,7 @@ CASES = [
     (128, 64, 4, 3, 1),
     (128, 128, 5, 4, 2),
     (256, 64, 5, 2, 3),
+    (256, 128, 2, 2, 0),  # coarsest level above 2048 dofs (65 x 33 nodes), replicated on both slabs
 ]
 
 
