@@ -143,6 +143,34 @@ __device__ __forceinline__ int stream_mis(const MarchArgs& a, const StreamDesc& 
   return static_cast<int>(p & 15u);
 }
 
+// CTA order of a pass. The hardware starts CTAs in increasing linear block
+// index (x fastest), so the columns a pass finishes with are the ones still
+// in L2 when the next pass starts. Stages that declare kReverse take their
+// tiles in the opposite order, so that a pass begins on the strips its
+// predecessor touched last: the fused update F, the residual + restriction
+// R | the prolongation + sweep R, the second post-sweep F, the direction
+// update R, and the next iteration's fused update F again. The logical tile
+// (and with it every reduction partial's index) does not change.
+#ifndef TMG_SERPENTINE
+#define TMG_SERPENTINE 1
+#endif
+template <class Stage, class = void>
+struct ReverseOf {
+  static constexpr bool value = false;
+};
+template <class Stage>
+struct ReverseOf<Stage, std::void_t<decltype(Stage::kReverse)>> {
+  static constexpr bool value = Stage::kReverse && TMG_SERPENTINE;
+};
+template <class Stage>
+__device__ __forceinline__ int tile_x() {
+  return ReverseOf<Stage>::value ? static_cast<int>(gridDim.x - 1 - blockIdx.x) : static_cast<int>(blockIdx.x);
+}
+template <class Stage>
+__device__ __forceinline__ int tile_y() {
+  return ReverseOf<Stage>::value ? static_cast<int>(gridDim.y - 1 - blockIdx.y) : static_cast<int>(blockIdx.y);
+}
+
 // ------------------------------------------------------------ node helpers --
 
 __device__ __forceinline__ uint32_t fixbits(uint32_t byte) {
@@ -499,6 +527,7 @@ using StSweep01U = StSweep01T<true>;
 // [X0, X0 + tx) and marches fine columns 2 X0 - 1 .. 2 (X0 + tx) - 1.
 struct StResidRestrict : WithF<-1> {
   static constexpr int kOwned = kTY - 2, kLead = 0;
+  static constexpr bool kReverse = true;
   // acc: this row's residual summed over the fine columns of the coarse
   // column being accumulated, with weights (1/2, 1, 1/2) in x; the rows are
   // combined ((1/2, 1, 1/2) in y) once per coarse column through smem
@@ -519,7 +548,7 @@ struct StResidRestrict : WithF<-1> {
       return;
     }
     // fine column 2X+1 closes coarse column X = (x-1)/2 and opens X+1
-    const int xlo = 2 * (blockIdx.y * a.tx) - 1;
+    const int xlo = 2 * (tile_y<StResidRestrict>() * a.tx) - 1;
     if (x != xlo) {
       acc.x = fma(0.5, r.x, acc.x);
       acc.y = fma(0.5, r.y, acc.y);
@@ -545,6 +574,7 @@ struct StResidRestrict : WithF<-1> {
 // previous entry's coarse column floor(c/2) from its (still held) slot.
 struct StProlongSweep : WithF<0> {
   static constexpr int NS = 5, kOwned = kTY, kLead = 1;
+  static constexpr bool kReverse = true;
   static constexpr int O_C = WithF<0>::kSlot;
   static constexpr int kSlot = O_C + sbytes(kTY / 2 + 3, 16);
   __device__ static StreamDesc stream(const MarchArgs& a, int k) {
@@ -623,6 +653,7 @@ struct StProlongSweep : WithF<0> {
 // comes from the device PCG state.
 struct StPupd {
   static constexpr int NS = 4, kRow0 = 0, kOwned = kTY, kLead = 0;
+  static constexpr bool kReverse = true;
   static constexpr int O_U = 0, O_E = O_U + sbytes(kTY + 2, 16), O_M = O_E + sbytes(kTY + 2, 8);
   static constexpr int O_P = O_M + sbytes(kTY + 2, 1);
   static constexpr int kSlot = O_P + sbytes(kTY + 2, 16);
@@ -683,14 +714,14 @@ struct RingOf<Stage, std::void_t<decltype(Stage::kRing)>> {
 template <class Stage>
 __device__ __forceinline__ void march_range(const MarchArgs& a, int& cf, int& cl, int& xlo, int& xhi) {
   if constexpr (Stage::kRow0 == -1) {
-    const int X0 = blockIdx.y * a.tx;
+    const int X0 = tile_y<Stage>() * a.tx;
     const int X1 = min(X0 + a.tx, a.gc.ncol);
     xlo = 2 * X0 - 1;
     xhi = 2 * X1 - 1;  // inclusive
     cf = xlo - 1;
     cl = xhi + 1;
   } else {
-    xlo = blockIdx.y * a.tx;
+    xlo = tile_y<Stage>() * a.tx;
     xhi = min(xlo + a.tx, a.g.ncol) - 1;
     cf = xlo - 1 - Stage::kLead;
     cl = xhi + 1;
@@ -705,7 +736,7 @@ __global__ void __launch_bounds__(kMarchThreads) k_march(MarchArgs a) {
 
   const Grid& g = a.g;
   const int t = threadIdx.x;
-  const int y0 = blockIdx.x * Stage::kOwned;
+  const int y0 = tile_x<Stage>() * Stage::kOwned;
   int cf, cl, xlo, xhi;
   march_range<Stage>(a, cf, cl, xlo, xhi);
   const int nent = cl - cf + 1;
@@ -820,7 +851,7 @@ __global__ void __launch_bounds__(kMarchThreads) k_march(MarchArgs a) {
   }
   if constexpr (RED) {
     static_assert(Stage::kOwned == kRedRows && Stage::kRow0 == 0, "reducing stages use the reduction tiles");
-    finish_reduction<kMarchThreads>(part, a.partials, blockIdx.x + gridDim.x * (a.rt.ctile0 + blockIdx.y), a.ticket,
+    finish_reduction<kMarchThreads>(part, a.partials, tile_x<Stage>() + gridDim.x * (a.rt.ctile0 + tile_y<Stage>()), a.ticket,
                                     gridDim.x * gridDim.y, a.rt.nparts, a.rop, a.st, a.hm, a.red_out);
   }
 }
