@@ -151,6 +151,9 @@ __device__ __forceinline__ int stream_mis(const MarchArgs& a, const StreamDesc& 
 // R | the prolongation + sweep R, the second post-sweep F, the direction
 // update R, and the next iteration's fused update F again. The logical tile
 // (and with it every reduction partial's index) does not change.
+#ifndef TMG_CLAMP_ROWS
+#define TMG_CLAMP_ROWS 1
+#endif
 #ifndef TMG_SERPENTINE
 #define TMG_SERPENTINE 1
 #endif
@@ -769,7 +772,13 @@ __global__ void __launch_bounds__(kMarchThreads) k_march(MarchArgs a) {
     for (int k = 0; k < Stage::NS; ++k) {
       const StreamDesc d = Stage::stream(a, k);
       mis[k] = stream_mis(a, d, y0);
-      bytes[k] = static_cast<uint32_t>((d.n * d.esize + mis[k] + 15) / 16 * 16);
+      // rows past ny + 2 feed no live node: the top row tile of a mesh with
+      // ny + 1 = 128 k + 1 rows (every BASELINE mesh) holds one live row and
+      // would stream 130 (1.5 % of a pass's traffic)
+      const int top = (d.coarse ? a.gc.ny : g.ny) + 2;
+      const int first = (d.coarse ? (y0 >> 1) : y0) + d.r0;
+      const int rows = TMG_CLAMP_ROWS ? max(1, min(d.n, top - first + 1)) : d.n;
+      bytes[k] = static_cast<uint32_t>((rows * d.esize + mis[k] + 15) / 16 * 16);
       total += bytes[k];
     }
     for (int j = 0; j < nent; ++j) {
