@@ -774,7 +774,8 @@ __global__ void __launch_bounds__(kMarchThreads) k_march(MarchArgs a) {
       mis[k] = stream_mis(a, d, y0);
       // rows past ny + 2 feed no live node: the top row tile of a mesh with
       // ny + 1 = 128 k + 1 rows (every BASELINE mesh) holds one live row and
-      // would stream 130 (1.5 % of a pass's traffic)
+      // would copy 130 (1.5 % of a pass's bulk-copy bytes, mostly L2 hits on
+      // the next column's first rows)
       const int top = (d.coarse ? a.gc.ny : g.ny) + 2;
       const int first = (d.coarse ? (y0 >> 1) : y0) + d.r0;
       const int rows = TMG_CLAMP_ROWS ? max(1, min(d.n, top - first + 1)) : d.n;
