@@ -65,7 +65,9 @@ typedef struct tmg_gpu_handle tmg_gpu_handle;
  * otherwise). Every BASELINE configuration coarsens to 8x8 = 162 dofs; the
  * reference default num_coarsenings = 2 (solvers.hpp:25) stays inside the
  * limit up to 256x256 or 512x256 elements. Above 2048 dofs the band is
- * factored in L2 and the handle holds three dense n x n arrays. */
+ * factored in L2 by one CTA and the handle holds three dense n x n arrays;
+ * such a level may have columns of at most 148 nodes (ny/2^nc + 1 <= 148,
+ * ConfigError otherwise), which keeps the factor around a second. */
 int tmg_gpu_create(int nx, int ny, int num_coarsenings, int dofs_per_node,
                    int device, tmg_gpu_handle** out);
 void tmg_gpu_destroy(tmg_gpu_handle* h);

@@ -1944,6 +1944,13 @@ int create_common(H* hp, int nx, int ny, int nc, int dpn, int device, int nranks
     return cfg("coarsest level has " + std::to_string(n0) + " dofs; the device coarse solve supports <= " +
                std::to_string(kCoarsestMaxDofs) + " (add coarsenings)");
   }
+  // the large-coarsest factor is one CTA walking the band: keep its b^2 n / 2
+  // updates around a second (129 x 65 or 65 x 129 coarsest nodes and smaller)
+  if (n0 > kDenseFactorMaxDofs && 2 * (ny / factor + 2) + 1 > kLargeCoarsestMaxBand) {
+    return cfg("coarsest level has " + std::to_string(n0) + " dofs in columns of " + std::to_string(ny / factor + 1) +
+               " nodes; above " + std::to_string(kDenseFactorMaxDofs) + " dofs the device coarse solve supports columns"
+               " of at most " + std::to_string((kLargeCoarsestMaxBand - 1) / 2 - 1) + " nodes (add coarsenings)");
+  }
   if (nranks < 1 || rank < 0 || rank >= nranks) return cfg("invalid rank / nranks");
   hp->device = device;
   hp->nx = nx;

@@ -704,6 +704,7 @@ __global__ void __launch_bounds__(kCholBandThreads) k_cholesky_band(double* __re
 // tiled kernels (k_cholesky_band_g, k_lower_inverse_band, k_gram_tiled).
 constexpr int kDenseFactorMaxDofs = 2048;
 constexpr int kCoarsestMaxDofs = 16900;
+constexpr int kLargeCoarsestMaxBand = 300;  // lower half-bandwidth (dofs) the one-CTA L2 band factor takes
 
 // Banded Cholesky of a large coarsest matrix (n > 2048: reference configs
 // with few coarsenings, e.g. 256^2 with the default num_coarsenings = 2,

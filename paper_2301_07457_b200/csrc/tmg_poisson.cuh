@@ -503,6 +503,11 @@ int tmg_poisson_create(int nx, int ny, int num_coarsenings, int device, tmg_pois
     if (n0 > kCoarsestMaxDofs)
       fail(TMG_ERR_CONFIG, "coarsest level has " + std::to_string(n0) + " dofs; at most " +
                                std::to_string(kCoarsestMaxDofs));
+    if (n0 > kDenseFactorMaxDofs && (ny >> num_coarsenings) + 2 > kLargeCoarsestMaxBand)
+      fail(TMG_ERR_CONFIG, "coarsest level has " + std::to_string(n0) + " dofs in columns of " +
+                               std::to_string((ny >> num_coarsenings) + 1) + " nodes; at most " +
+                               std::to_string(kLargeCoarsestMaxBand - 1) + " above " +
+                               std::to_string(kDenseFactorMaxDofs) + " dofs");
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->lev.resize(num_coarsenings + 1);
     for (int l = 0; l <= num_coarsenings; ++l) {

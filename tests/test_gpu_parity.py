@@ -540,6 +540,9 @@ def test_large_coarsest_level_singular_and_limit():
         free.set_moduli(np.ones(128 * 128))
     with pytest.raises(P.ConfigError):
         P.MultigridOperators(P.GridLevel(512, 512), 2, 0.3, P.BoundaryConditions([], []))
+    # a tall coarsest level (2 x 2049 nodes): the one-CTA band factor would run for minutes
+    with pytest.raises(P.ConfigError):
+        P.MultigridOperators(P.GridLevel(2, 4096), 1, 0.3, P.BoundaryConditions([], []))
 
 
 @pytest.mark.parametrize("nx,ny,nc", [(64, 64, 3), (128, 96, 3), (160, 96, 4)])
