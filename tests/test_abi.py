@@ -112,6 +112,12 @@ def test_config_errors_precede_device_work():
         P.MultigridOperators(P.GridLevel(10, 8), 2, 0.3, P.BoundaryConditions())
     with pytest.raises(P.ConfigError):
         P.MultigridOperators(P.GridLevel(0, 8), 0, 0.3, P.BoundaryConditions())
+    # the documented limits of the device coarse solve (include/tmg_gpu.h): at
+    # most 16,900 coarsest dofs, and above 2048 dofs node columns of <= 148 nodes
+    with pytest.raises(P.ConfigError, match="16900"):
+        P.MultigridOperators(P.GridLevel(512, 512), 2, 0.3, P.BoundaryConditions())
+    with pytest.raises(P.ConfigError, match="148 nodes"):
+        P.MultigridOperators(P.GridLevel(2, 4096), 1, 0.3, P.BoundaryConditions())
 
 
 def test_boundary_condition_validation_mirrors_reference():
