@@ -153,8 +153,10 @@ __global__ void __launch_bounds__(kOcThreads) k_oc_gain(OcArgs a, int prep_block
   const bool half = a.damping == 0.5;
   for (long e = blockIdx.x * static_cast<long>(kOcThreads) + threadIdx.x; e < a.ne;
        e += static_cast<long>(gridDim.x) * kOcThreads) {
-    const double g = s_max(floor_gain, a.el0[e].y);
-    a.el0[e].y = half ? sqrt(g) : log(g);
+    double2 v = a.el0[e];  // whole 16-byte record in and out: full sectors both ways
+    const double g = s_max(floor_gain, v.y);
+    v.y = half ? sqrt(g) : log(g);
+    a.el0[e] = v;
   }
 }
 
